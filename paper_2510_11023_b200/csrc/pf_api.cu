@@ -1,0 +1,738 @@
+// C-ABI of the B200 parareal fine-propagator path (include/parafrac_b200.h).
+//
+// Host side of the drop-in boundary: context (tables, buffers, stream),
+// kernel dispatch per space, status decoding into the reference's error
+// conventions (errors.py:8-34), and the on-device parareal state machine
+// (parareal.py:91-155).  No CPU compute path exists: every entry point that
+// computes launches sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/parafrac_b200.h"
+#include "pf_cheb1d.cuh"
+#include "pf_device.cuh"
+#include "pf_kernels.cuh"
+#include "pf_sine1d.cuh"
+
+using pf::cd;
+using pf::Status;
+
+namespace {
+
+enum Variant { V_NONE = 0, V_SINE_128_1, V_SINE_256_1, V_SINE_256_2, V_SINE_256_4, V_CHEB_128_1 };
+
+struct DevBuf {
+  double* p = nullptr;
+  size_t n = 0;  // doubles
+  int ensure(size_t want) {
+    if (want <= n) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (cudaMalloc(&p, want * sizeof(double)) != cudaSuccess) return -1;
+    n = want;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+struct pf_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  pf_problem prob{};
+  pf_grid grid{};
+  int kind = 0, size = 0, M = 0, Q = 0, lgQ = 0, npts = 0, ni = 0;
+  double dT = 0, dt = 0, gam_f = 0, gam_c = 0, minv = 0, g2m = 0;
+  double pcg_tol = 1e-14;
+  int pcg_maxit = 500;
+  Variant variant = V_NONE;
+  size_t smem = 0;
+  std::vector<double> h_bfine, h_bfrac, h_nodes, h_d1, h_qw;
+  // device tables
+  double *d_bfine = nullptr, *d_afine = nullptr, *d_bfrac = nullptr, *d_nodes = nullptr, *d_d1 = nullptr, *d_qw = nullptr;
+  cd *d_tw = nullptr, *d_ph = nullptr;
+  long len_fine = 0, len_frac = 0;
+  // work buffers
+  DevBuf U, Unext, paths, fold, gold, gnew, io, scalar, scratch;
+  Status* d_status = nullptr;
+  int status_cap = 0;
+  std::vector<Status> h_status;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  pf_stats stats{};
+  pf_error err{};
+  double guard = 0;
+  bool parareal_ready = false;
+};
+
+namespace {
+
+int set_error(pf_ctx* c, int code, const char* msg) {
+  c->err.code = code;
+  std::snprintf(c->err.message, sizeof(c->err.message), "%s", msg);
+  return code;
+}
+
+int cuda_fail(pf_ctx* c, cudaError_t e, const char* where) {
+  c->err = pf_error{};
+  c->err.code = PF_ERR_CUDA;
+  c->err.cuda_error = (int)e;
+  std::snprintf(c->err.message, sizeof(c->err.message), "%s: %s", where, cudaGetErrorString(e));
+  return PF_ERR_CUDA;
+}
+
+#define PF_CUDA(ctx, call)                                   \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #call); \
+  } while (0)
+
+bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+pf::Common make_common(const pf_ctx* c) {
+  pf::Common cm{};
+  cm.fn.id = c->prob.functor;
+  for (int i = 0; i < 6; ++i) cm.fn.p[i] = c->prob.p[i];
+  cm.size = c->size;
+  cm.nt = c->grid.nt;
+  cm.m = c->grid.m;
+  cm.dT = c->dT;
+  cm.dt = c->dt;
+  cm.gam_f = c->gam_f;
+  cm.gam_c = c->gam_c;
+  cm.minv = c->minv;
+  cm.bfine = c->d_bfine;
+  cm.afine = c->d_afine;
+  cm.bfrac = c->d_bfrac;
+  cm.scratch = c->scratch.p;
+  return cm;
+}
+
+pf::Sine1DParams sine_params(const pf_ctx* c) {
+  pf::Sine1DParams p{};
+  p.M = c->M;
+  p.Q = c->Q;
+  p.lgQ = c->lgQ;
+  p.tw = c->d_tw;
+  p.ph = c->d_ph;
+  p.pcg_tol = c->pcg_tol;
+  p.pcg_maxit = c->pcg_maxit;
+  return p;
+}
+
+pf::Cheb1DParams cheb_params(const pf_ctx* c) {
+  pf::Cheb1DParams p{};
+  p.npts = c->npts;
+  p.ni = c->ni;
+  p.nodes = c->d_nodes;
+  p.d1 = c->d_d1;
+  p.qw = c->d_qw;
+  return p;
+}
+
+// Dispatch: binds SP (space type), SPP (its params), NT, EPT and `spp`.
+#define PF_DISPATCH(ctx, ...)                                        \
+  switch ((ctx)->variant) {                                          \
+    case V_SINE_128_1: {                                             \
+      using SP = pf::Sine1D<128, 1>;                                 \
+      using SPP = pf::Sine1DParams;                                  \
+      constexpr int NT = 128, EPT = 1;                               \
+      SPP spp = sine_params(ctx);                                    \
+      __VA_ARGS__;                                                   \
+    } break;                                                         \
+    case V_SINE_256_1: {                                             \
+      using SP = pf::Sine1D<256, 1>;                                 \
+      using SPP = pf::Sine1DParams;                                  \
+      constexpr int NT = 256, EPT = 1;                               \
+      SPP spp = sine_params(ctx);                                    \
+      __VA_ARGS__;                                                   \
+    } break;                                                         \
+    case V_SINE_256_2: {                                             \
+      using SP = pf::Sine1D<256, 2>;                                 \
+      using SPP = pf::Sine1DParams;                                  \
+      constexpr int NT = 256, EPT = 2;                               \
+      SPP spp = sine_params(ctx);                                    \
+      __VA_ARGS__;                                                   \
+    } break;                                                         \
+    case V_SINE_256_4: {                                             \
+      using SP = pf::Sine1D<256, 4>;                                 \
+      using SPP = pf::Sine1DParams;                                  \
+      constexpr int NT = 256, EPT = 4;                               \
+      SPP spp = sine_params(ctx);                                    \
+      __VA_ARGS__;                                                   \
+    } break;                                                         \
+    case V_CHEB_128_1: {                                             \
+      using SP = pf::Cheb1D<128, 1>;                                 \
+      using SPP = pf::Cheb1DParams;                                  \
+      constexpr int NT = 128, EPT = 1;                               \
+      SPP spp = cheb_params(ctx);                                    \
+      __VA_ARGS__;                                                   \
+    } break;                                                         \
+    default:                                                         \
+      return set_error(ctx, PF_ERR_UNSUPPORTED, "no kernel variant"); \
+  }
+
+int ensure_status(pf_ctx* c, int n) {
+  if (n <= c->status_cap) return 0;
+  if (c->d_status) cudaFree(c->d_status);
+  c->d_status = nullptr;
+  c->status_cap = 0;
+  PF_CUDA(c, cudaMalloc(&c->d_status, sizeof(Status) * n));
+  c->status_cap = n;
+  c->h_status.resize(n);
+  return 0;
+}
+
+// Launch the fine sweep for slices [n_lo, n_lo+bs) reading device states d_u.
+int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, Status* d_st) {
+  if (c->paths.ensure((size_t)bs * (c->grid.m + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "paths");
+  if (c->scratch.ensure((size_t)bs * 2 * pf::HB * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
+  pf::Common cm = make_common(c);
+  double* dp = c->paths.p;
+  PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+  PF_DISPATCH(c, {
+    auto kern = pf::k_fine_sweep<SP, SPP, NT, EPT>;
+    PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
+    kern<<<bs, NT, c->smem, c->stream>>>(cm, spp, d_u, n_lo, dp, d_out, d_st);
+  });
+  PF_CUDA(c, cudaGetLastError());
+  PF_CUDA(c, cudaEventRecord(c->ev1, c->stream));
+  c->stats.fine_launches += 1;
+  return 0;
+}
+
+int launch_coarse(pf_ctx* c, const pf::CoarseArgs& a, Status* d_st) {
+  pf::Common cm = make_common(c);
+  PF_DISPATCH(c, {
+    auto kern = pf::k_coarse<SP, SPP, NT, EPT>;
+    PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
+    kern<<<1, NT, c->smem, c->stream>>>(cm, spp, a, d_st);
+  });
+  PF_CUDA(c, cudaGetLastError());
+  c->stats.coarse_launches += 1;
+  return 0;
+}
+
+// Decode a fine-sweep status array: the earliest substep r fails first;
+// at equal r a coefficient error precedes the solve (stepping.py:225-241).
+int decode_fine(pf_ctx* c, int n_lo, int count) {
+  PF_CUDA(c, cudaMemcpyAsync(c->h_status.data(), c->d_status, sizeof(Status) * count, cudaMemcpyDeviceToHost,
+                             c->stream));
+  PF_CUDA(c, cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, c->ev0, c->ev1) == cudaSuccess) c->stats.last_fine_ms = ms;
+  int best = -1;
+  for (int i = 0; i < count; ++i) {
+    const Status& s = c->h_status[i];
+    c->stats.pcg_iterations += s.iters;
+    c->stats.solves += s.solves;
+    if (s.code == pf::ST_OK) continue;
+    if (best < 0) {
+      best = i;
+      continue;
+    }
+    const Status& b = c->h_status[best];
+    if (s.r < b.r || (s.r == b.r && s.code == pf::ST_COEFF && b.code != pf::ST_COEFF)) best = i;
+  }
+  if (best < 0) return 0;
+  const Status& s = c->h_status[best];
+  c->err = pf_error{};
+  c->err.step_n = n_lo;
+  c->err.step_r = s.r;
+  if (s.code == pf::ST_COEFF) {
+    c->err.code = PF_ERR_COEFFICIENT;
+    c->err.node = s.node;
+    std::snprintf(c->err.message, sizeof(c->err.message), "diffusion coefficient is not finite");
+  } else {
+    c->err.code = PF_ERR_SOLVER;
+    std::snprintf(c->err.message, sizeof(c->err.message), "fine-sweep solve failed (interval %d)", s.n);
+  }
+  return c->err.code;
+}
+
+int decode_coarse(pf_ctx* c, int step_offset, int k_iter) {
+  PF_CUDA(c, cudaMemcpyAsync(c->h_status.data(), c->d_status, sizeof(Status), cudaMemcpyDeviceToHost, c->stream));
+  PF_CUDA(c, cudaStreamSynchronize(c->stream));
+  const Status& s = c->h_status[0];
+  c->stats.pcg_iterations += s.iters;
+  c->stats.solves += s.solves;
+  if (s.code == pf::ST_OK) return 0;
+  c->err = pf_error{};
+  c->err.step_r = -1;
+  if (s.code == pf::ST_COEFF) {
+    c->err.code = PF_ERR_COEFFICIENT;
+    c->err.node = s.node;
+    c->err.step_n = s.n + step_offset;
+    std::snprintf(c->err.message, sizeof(c->err.message), "diffusion coefficient is not finite");
+  } else if (s.code == pf::ST_DIVERGE) {
+    c->err.code = PF_ERR_DIVERGENCE;
+    c->err.iteration = k_iter;
+    c->err.interval = s.n;
+    std::snprintf(c->err.message, sizeof(c->err.message), "%s",
+                  s.r == 0 ? "non-finite state after correction sweep" : "state norm exceeds divergence guard");
+  } else {
+    c->err.code = PF_ERR_SOLVER;
+    c->err.step_n = s.n + step_offset;
+    std::snprintf(c->err.message, sizeof(c->err.message), "singular or ill-conditioned time-step system");
+  }
+  return c->err.code;
+}
+
+double host_norm(const pf_ctx* c, const double* v) {
+  double s = 0.0;
+  if (c->kind == PF_SPACE_CHEB1D) {
+    for (int i = 0; i < c->ni; ++i) s += c->h_qw[i + 1] * v[i] * v[i];
+  } else {
+    for (int i = 0; i < c->size; ++i) s += v[i] * v[i];
+  }
+  return std::sqrt(s);
+}
+
+int upload(pf_ctx* c, double* dst, const double* src, size_t n) {
+  PF_CUDA(c, cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  return 0;
+}
+int download(pf_ctx* c, double* dst, const double* src, size_t n) {
+  PF_CUDA(c, cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  return 0;
+}
+
+double l1_formula(double x, double alpha) {
+  if (alpha == 1.0) return x == 0.0 ? 1.0 : 0.0;
+  const double e = 1.0 - alpha;
+  return std::pow(x + 1.0, e) - std::pow(x, e);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pf_version(void) { return "parafrac_b200 0.1.0 (sm_100a)"; }
+
+int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* space, const pf_weights* weights,
+              int device, pf_ctx** out) {
+  if (!out) return PF_ERR_ARGUMENT;
+  *out = nullptr;
+  pf_ctx* c = new pf_ctx();
+  *out = c;
+  if (!problem || !grid || !space) return set_error(c, PF_ERR_ARGUMENT, "null argument");
+  c->prob = *problem;
+  c->grid = *grid;
+  if (!(problem->alpha > 0.0 && problem->alpha <= 1.0))
+    return set_error(c, PF_ERR_ARGUMENT, "fractional order must lie in (0, 1]");
+  if (!(problem->t_final > 0.0)) return set_error(c, PF_ERR_ARGUMENT, "final time must be positive");
+  if (grid->nt < 1 || grid->m < 1) return set_error(c, PF_ERR_ARGUMENT, "grid counts nt and m must be positive integers");
+  if (problem->functor < 1 || problem->functor > 5) return set_error(c, PF_ERR_UNSUPPORTED, "unknown coefficient functor");
+  c->kind = space->kind;
+  c->pcg_tol = space->pcg_tol > 0 ? space->pcg_tol : 1e-14;
+  c->pcg_maxit = space->pcg_maxit > 0 ? space->pcg_maxit : 500;
+  if (space->kind == PF_SPACE_SINE1D) {
+    const int M = space->modes;
+    if (!is_pow2(M) || M > 1024) return set_error(c, PF_ERR_UNSUPPORTED, "sine modes must be a power of two <= 1024");
+    c->M = M;
+    c->Q = 2 * M;
+    c->lgQ = 0;
+    while ((1 << c->lgQ) < c->Q) ++c->lgQ;
+    c->size = M;
+    c->variant = M <= 128 ? V_SINE_128_1 : M <= 256 ? V_SINE_256_1 : M <= 512 ? V_SINE_256_2 : V_SINE_256_4;
+    c->smem = pf::Sine1D<256, 1>::smem_bytes(M);
+  } else if (space->kind == PF_SPACE_CHEB1D) {
+    const int deg = space->modes;
+    if (deg < 2) return set_error(c, PF_ERR_ARGUMENT, "degree must be at least 2 so interior nodes exist");
+    if (!space->nodes || !space->d1 || !space->quad_weights)
+      return set_error(c, PF_ERR_ARGUMENT, "Chebyshev space needs nodes, d1 and quad_weights");
+    c->npts = deg + 1;
+    c->ni = deg - 1;
+    c->size = c->ni;
+    c->smem = pf::Cheb1D<128, 1>::smem_bytes(deg);
+    if (c->ni > 128 || c->smem > 227 * 1024)
+      return set_error(c, PF_ERR_UNSUPPORTED, "Chebyshev bridge supports degree <= ~100 (shared-memory resident)");
+    c->variant = V_CHEB_128_1;
+    c->h_nodes.assign(space->nodes, space->nodes + c->npts);
+    c->h_d1.assign(space->d1, space->d1 + (size_t)c->npts * c->npts);
+    c->h_qw.assign(space->quad_weights, space->quad_weights + c->npts);
+  } else {
+    return set_error(c, PF_ERR_UNSUPPORTED, "space kind not built in this library");
+  }
+  const double alpha = problem->alpha;
+  const int nt = grid->nt, m = grid->m;
+  c->dT = problem->t_final / nt;
+  c->dt = c->dT / m;
+  c->g2m = (weights && weights->gamma_2_minus > 0) ? weights->gamma_2_minus : std::exp(std::lgamma(2.0 - alpha));
+  c->gam_f = std::pow(c->dt, alpha) * c->g2m;
+  c->gam_c = std::pow(c->dT, alpha) * c->g2m;
+  c->minv = std::pow((double)m, -alpha);
+  // weight tables (caller's rounding when given, libm pow otherwise)
+  const long need_fine = std::max<long>((long)nt * m + 1, std::max(m, nt) + 2) + pf::HB;  // + block padding
+  const long need_frac = (long)(nt > 1 ? nt - 1 : 0) * m + m + 1 + pf::HB;
+  c->h_bfine.resize(need_fine);
+  c->h_bfrac.resize(need_frac);
+  for (long q = 0; q < need_fine; ++q) {
+    if (weights && weights->b_fine && q < weights->len_fine)
+      c->h_bfine[q] = weights->b_fine[q];
+    else
+      c->h_bfine[q] = l1_formula((double)q, alpha);
+  }
+  for (long q = 0; q < need_frac; ++q) {
+    if (weights && weights->b_frac && q < weights->len_frac)
+      c->h_bfrac[q] = weights->b_frac[q];
+    else
+      c->h_bfrac[q] = l1_formula((double)q / (double)m, alpha);
+  }
+  c->len_fine = need_fine;
+  std::vector<double> h_afine(need_fine + pf::HB + 1, 0.0);
+  for (long s = 1; s < need_fine; ++s) h_afine[s] = c->h_bfine[s - 1] - c->h_bfine[s];
+  c->len_frac = need_frac;
+
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaSetDevice");
+  PF_CUDA(c, cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+  c->stream = c->own_stream;
+  PF_CUDA(c, cudaEventCreate(&c->ev0));
+  PF_CUDA(c, cudaEventCreate(&c->ev1));
+  PF_CUDA(c, cudaMalloc(&c->d_bfine, sizeof(double) * need_fine));
+  PF_CUDA(c, cudaMalloc(&c->d_bfrac, sizeof(double) * need_frac));
+  PF_CUDA(c, cudaMemcpy(c->d_bfine, c->h_bfine.data(), sizeof(double) * need_fine, cudaMemcpyHostToDevice));
+  PF_CUDA(c, cudaMalloc(&c->d_afine, sizeof(double) * h_afine.size()));
+  PF_CUDA(c, cudaMemcpy(c->d_afine, h_afine.data(), sizeof(double) * h_afine.size(), cudaMemcpyHostToDevice));
+  PF_CUDA(c, cudaMemcpy(c->d_bfrac, c->h_bfrac.data(), sizeof(double) * need_frac, cudaMemcpyHostToDevice));
+  if (c->kind == PF_SPACE_SINE1D) {
+    std::vector<cd> tw(c->Q), ph(c->Q);
+    const long double PI = 3.141592653589793238462643383279502884L;
+    for (int j = 0; j < c->Q; ++j) {
+      const long double a = -2.0L * PI * (long double)j / (long double)c->Q;
+      tw[j] = {(double)cosl(a), (double)sinl(a)};
+      const long double b = PI * (long double)j / (2.0L * (long double)c->Q);
+      ph[j] = {(double)cosl(b), (double)sinl(b)};
+    }
+    PF_CUDA(c, cudaMalloc(&c->d_tw, sizeof(cd) * c->Q));
+    PF_CUDA(c, cudaMalloc(&c->d_ph, sizeof(cd) * c->Q));
+    PF_CUDA(c, cudaMemcpy(c->d_tw, tw.data(), sizeof(cd) * c->Q, cudaMemcpyHostToDevice));
+    PF_CUDA(c, cudaMemcpy(c->d_ph, ph.data(), sizeof(cd) * c->Q, cudaMemcpyHostToDevice));
+  } else {
+    PF_CUDA(c, cudaMalloc(&c->d_nodes, sizeof(double) * c->npts));
+    PF_CUDA(c, cudaMalloc(&c->d_d1, sizeof(double) * c->npts * c->npts));
+    PF_CUDA(c, cudaMalloc(&c->d_qw, sizeof(double) * c->npts));
+    PF_CUDA(c, cudaMemcpy(c->d_nodes, c->h_nodes.data(), sizeof(double) * c->npts, cudaMemcpyHostToDevice));
+    PF_CUDA(c, cudaMemcpy(c->d_d1, c->h_d1.data(), sizeof(double) * c->npts * c->npts, cudaMemcpyHostToDevice));
+    PF_CUDA(c, cudaMemcpy(c->d_qw, c->h_qw.data(), sizeof(double) * c->npts, cudaMemcpyHostToDevice));
+  }
+  if (ensure_status(c, std::max(nt, 1))) return c->err.code;
+  c->err = pf_error{};
+  return PF_OK;
+}
+
+void pf_destroy(pf_ctx* c) {
+  if (!c) return;
+  if (c->device >= 0) cudaSetDevice(c->device);
+  for (DevBuf* b : {&c->U, &c->Unext, &c->paths, &c->fold, &c->gold, &c->gnew, &c->io, &c->scalar, &c->scratch}) b->release();
+  for (void* p : {(void*)c->d_bfine, (void*)c->d_afine, (void*)c->d_bfrac, (void*)c->d_nodes, (void*)c->d_d1, (void*)c->d_qw,
+                  (void*)c->d_tw, (void*)c->d_ph, (void*)c->d_status})
+    if (p) cudaFree(p);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+}
+
+int pf_last_error(const pf_ctx* c, pf_error* out) {
+  if (!c || !out) return PF_ERR_ARGUMENT;
+  *out = c->err;
+  return PF_OK;
+}
+
+int pf_state_size(const pf_ctx* c) { return c ? c->size : -1; }
+
+int pf_get_stats(const pf_ctx* c, pf_stats* out) {
+  if (!c || !out) return PF_ERR_ARGUMENT;
+  *out = c->stats;
+  return PF_OK;
+}
+
+int pf_reset_stats(pf_ctx* c) {
+  if (!c) return PF_ERR_ARGUMENT;
+  c->stats = pf_stats{};
+  return PF_OK;
+}
+
+int pf_set_stream(pf_ctx* c, void* stream) {
+  if (!c) return PF_ERR_ARGUMENT;
+  c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+  return PF_OK;
+}
+
+int pf_dev_fine_sweep_async(pf_ctx* c, const double* d_u, int n_lo, int n_hi, double* d_out) {
+  if (!c) return PF_ERR_ARGUMENT;
+  const int bs = n_hi - n_lo;
+  if (bs < 1 || n_lo < 0 || n_hi > c->grid.nt) return set_error(c, PF_ERR_ARGUMENT, "interval range outside the supplied coarse states");
+  cudaSetDevice(c->device);
+  if (ensure_status(c, bs)) return c->err.code;
+  return launch_fine(c, d_u, n_lo, bs, d_out, c->d_status);
+}
+
+int pf_dev_fine_sweep(pf_ctx* c, const double* d_u, int n_lo, int n_hi, double* d_out) {
+  int rc = pf_dev_fine_sweep_async(c, d_u, n_lo, n_hi, d_out);
+  if (rc) return rc;
+  return decode_fine(c, n_lo, n_hi - n_lo);
+}
+
+int pf_dev_check(pf_ctx* c) {
+  if (!c) return PF_ERR_ARGUMENT;
+  PF_CUDA(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int pf_fine_sweep(pf_ctx* c, const double* u_nodes, int n_states, int n_lo, int n_hi, double* out) {
+  if (!c || !u_nodes || !out) return PF_ERR_ARGUMENT;
+  const int bs = n_hi - n_lo;
+  if (bs < 1 || n_lo < 0 || n_hi > n_states - 1 || n_hi > c->grid.nt)
+    return set_error(c, PF_ERR_ARGUMENT, "interval range outside the supplied coarse states");
+  cudaSetDevice(c->device);
+  if (c->io.ensure((size_t)(n_hi + bs) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "io");
+  double* d_u = c->io.p;
+  double* d_out = c->io.p + (size_t)n_hi * c->size;
+  if (upload(c, d_u, u_nodes, (size_t)n_hi * c->size)) return c->err.code;
+  if (ensure_status(c, bs)) return c->err.code;
+  int rc = launch_fine(c, d_u, n_lo, bs, d_out, c->d_status);
+  if (rc) return rc;
+  if (download(c, out, d_out, (size_t)bs * c->size)) return c->err.code;
+  return decode_fine(c, n_lo, bs);
+}
+
+int pf_fine_propagate(pf_ctx* c, const double* hist, int n_states, double* endpoint, double* path) {
+  if (!c || !hist || n_states < 1) return PF_ERR_ARGUMENT;
+  const int n = n_states - 1;
+  if (n >= c->grid.nt) return set_error(c, PF_ERR_ARGUMENT, "interval index outside the grid");
+  cudaSetDevice(c->device);
+  if (c->io.ensure((size_t)(n_states + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "io");
+  double* d_u = c->io.p;
+  double* d_out = c->io.p + (size_t)n_states * c->size;
+  if (upload(c, d_u, hist, (size_t)n_states * c->size)) return c->err.code;
+  int rc = launch_fine(c, d_u, n, 1, d_out, c->d_status);
+  if (rc) return rc;
+  if (endpoint && download(c, endpoint, d_out, c->size)) return c->err.code;
+  if (path && download(c, path, c->paths.p + c->size, (size_t)c->grid.m * c->size)) return c->err.code;
+  return decode_fine(c, n, 1);
+}
+
+int pf_coarse_step(pf_ctx* c, const double* history, int n_states, int step_index, double* out) {
+  if (!c || !history || !out || n_states < 1) return c ? set_error(c, PF_ERR_ARGUMENT, "history must be a nonempty stack of states") : PF_ERR_ARGUMENT;
+  const int n = n_states - 1;
+  if (n + 1 >= c->len_fine) return set_error(c, PF_ERR_ARGUMENT, "history longer than the weight tables");
+  cudaSetDevice(c->device);
+  if (c->io.ensure((size_t)(n_states + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "io");
+  if (upload(c, c->io.p, history, (size_t)n_states * c->size)) return c->err.code;
+  pf::CoarseArgs a{};
+  a.mode = pf::CM_SINGLE;
+  a.n_single = n;
+  a.traj = c->io.p;
+  a.out = c->io.p + (size_t)n_states * c->size;
+  int rc = launch_coarse(c, a, c->d_status);
+  if (rc) return rc;
+  if (download(c, out, a.out, c->size)) return c->err.code;
+  rc = decode_coarse(c, 0, 0);
+  if (rc == PF_ERR_SOLVER || rc == PF_ERR_COEFFICIENT) c->err.step_n = step_index;
+  return rc;
+}
+
+static int run_coarse_dev(pf_ctx* c, double* d_traj) {
+  pf::CoarseArgs a{};
+  a.mode = pf::CM_RUN;
+  a.traj = d_traj;
+  int rc = launch_coarse(c, a, c->d_status);
+  if (rc) return rc;
+  return decode_coarse(c, 0, 0);
+}
+
+int pf_run_coarse(pf_ctx* c, const double* u0, double* traj) {
+  if (!c || !u0 || !traj) return PF_ERR_ARGUMENT;
+  cudaSetDevice(c->device);
+  const size_t rows = (size_t)c->grid.nt + 1;
+  if (c->io.ensure(rows * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "io");
+  if (upload(c, c->io.p, u0, c->size)) return c->err.code;
+  int rc = run_coarse_dev(c, c->io.p);
+  if (rc) return rc;
+  if (download(c, traj, c->io.p, rows * c->size)) return c->err.code;
+  PF_CUDA(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int pf_chain_fine(pf_ctx* c, const double* u0, double* traj) {
+  if (!c || !u0 || !traj) return PF_ERR_ARGUMENT;
+  cudaSetDevice(c->device);
+  const int nt = c->grid.nt;
+  const size_t rows = (size_t)nt + 1;
+  if (c->io.ensure(rows * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "io");
+  if (upload(c, c->io.p, u0, c->size)) return c->err.code;
+  if (ensure_status(c, nt)) return c->err.code;
+  for (int n = 0; n < nt; ++n) {
+    int rc = launch_fine(c, c->io.p, n, 1, c->io.p + (size_t)(n + 1) * c->size, c->d_status + n);
+    if (rc) return rc;
+  }
+  PF_CUDA(c, cudaMemcpyAsync(c->h_status.data(), c->d_status, sizeof(Status) * nt, cudaMemcpyDeviceToHost, c->stream));
+  if (download(c, traj, c->io.p, rows * c->size)) return c->err.code;
+  PF_CUDA(c, cudaStreamSynchronize(c->stream));
+  for (int n = 0; n < nt; ++n) {
+    const Status& s = c->h_status[n];
+    c->stats.pcg_iterations += s.iters;
+    c->stats.solves += s.solves;
+    if (s.code != pf::ST_OK) {
+      c->err = pf_error{};
+      c->err.code = s.code == pf::ST_COEFF ? PF_ERR_COEFFICIENT : PF_ERR_SOLVER;
+      c->err.step_n = n;
+      c->err.step_r = s.r;
+      c->err.node = s.node;
+      std::snprintf(c->err.message, sizeof(c->err.message), "chain_fine failed in interval %d", n);
+      return c->err.code;
+    }
+  }
+  return 0;
+}
+
+int pf_fine_sequential(pf_ctx* c, const double* u0, double* states) {
+  if (!c || !u0 || !states) return PF_ERR_ARGUMENT;
+  cudaSetDevice(c->device);
+  const long total = (long)c->grid.nt * c->grid.m;
+  if (c->len_fine < total + 1) return set_error(c, PF_ERR_ARGUMENT, "weight table shorter than nt*m+1");
+  if (c->paths.ensure((size_t)(total + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "hist");
+  if (upload(c, c->paths.p, u0, c->size)) return c->err.code;
+  pf::Common cm = make_common(c);
+  double* dh = c->paths.p;
+  PF_DISPATCH(c, {
+    auto kern = pf::k_sequential<SP, SPP, NT, EPT>;
+    PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
+    kern<<<1, NT, c->smem, c->stream>>>(cm, spp, dh, (int)total, c->d_status);
+  });
+  PF_CUDA(c, cudaGetLastError());
+  for (int n = 0; n <= c->grid.nt; ++n)
+    if (download(c, states + (size_t)n * c->size, dh + (size_t)n * c->grid.m * c->size, c->size)) return c->err.code;
+  int rc = decode_coarse(c, 0, 0);
+  return rc;
+}
+
+int pf_dev_parareal_init(pf_ctx* c, const double* u0) {
+  if (!c || !u0) return PF_ERR_ARGUMENT;
+  cudaSetDevice(c->device);
+  const size_t rows = (size_t)c->grid.nt + 1, sz = c->size;
+  for (DevBuf* b : {&c->U, &c->Unext}) if (b->ensure(rows * sz)) return cuda_fail(c, cudaErrorMemoryAllocation, "U");
+  for (DevBuf* b : {&c->fold, &c->gold, &c->gnew}) if (b->ensure((rows - 1) * sz)) return cuda_fail(c, cudaErrorMemoryAllocation, "G");
+  if (c->scalar.ensure(8)) return cuda_fail(c, cudaErrorMemoryAllocation, "scalar");
+  if (upload(c, c->U.p, u0, sz)) return c->err.code;
+  int rc = run_coarse_dev(c, c->U.p);
+  if (rc) return rc;
+  // G_old at k = 0 equals the coarse trajectory (parareal.py:78-79 == stepping.py:119-120)
+  PF_CUDA(c, cudaMemcpyAsync(c->gold.p, c->U.p + sz, (rows - 1) * sz * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  c->guard = 1e12 * std::max(host_norm(c, u0), 1.0);  // parareal.py:98
+  c->parareal_ready = true;
+  return 0;
+}
+
+const double* pf_dev_parareal_states(pf_ctx* c) { return c ? c->U.p : nullptr; }
+
+int pf_dev_parareal_correct(pf_ctx* c, const double* d_fold, int k, double* diff) {
+  if (!c || !c->parareal_ready) return c ? set_error(c, PF_ERR_ARGUMENT, "parareal state not initialised") : PF_ERR_ARGUMENT;
+  cudaSetDevice(c->device);
+  pf::CoarseArgs a{};
+  a.mode = pf::CM_CORRECT;
+  a.k_iter = k;
+  a.guard = c->guard;
+  a.ucur = c->U.p;
+  a.fold = d_fold ? d_fold : c->fold.p;
+  a.gold = c->gold.p;
+  a.gnew = c->gnew.p;
+  a.unext = c->Unext.p;
+  a.out = c->scalar.p;
+  // From the second iteration on, G_old is the previous sweep's G_new, which
+  // is bitwise what parareal.py:78-79 recomputes.
+  if (k > 0) std::swap(c->gold, c->gnew);
+  a.gold = c->gold.p;
+  a.gnew = c->gnew.p;
+  if (d_fold && d_fold != c->fold.p)
+    PF_CUDA(c, cudaMemcpyAsync(c->fold.p, d_fold, (size_t)c->grid.nt * c->size * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  float ms = 0.f;
+  PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+  int rc = launch_coarse(c, a, c->d_status);
+  if (rc) return rc;
+  PF_CUDA(c, cudaEventRecord(c->ev1, c->stream));
+  double h = 0.0;
+  PF_CUDA(c, cudaMemcpyAsync(&h, c->scalar.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  rc = decode_coarse(c, 0, k);
+  if (cudaEventElapsedTime(&ms, c->ev0, c->ev1) == cudaSuccess) c->stats.last_coarse_ms = ms;
+  if (rc) return rc;
+  if (diff) *diff = h;
+  std::swap(c->U, c->Unext);  // u_curr = u_next (parareal.py:133)
+  return 0;
+}
+
+int pf_dev_parareal_read(pf_ctx* c, double* states, double* coarse_new, double* coarse_old) {
+  if (!c) return PF_ERR_ARGUMENT;
+  const size_t rows = (size_t)c->grid.nt + 1, sz = c->size;
+  if (states && download(c, states, c->U.p, rows * sz)) return c->err.code;
+  if (coarse_new && download(c, coarse_new, c->gnew.p, (rows - 1) * sz)) return c->err.code;
+  if (coarse_old && download(c, coarse_old, c->gold.p, (rows - 1) * sz)) return c->err.code;
+  PF_CUDA(c, cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int pf_parareal(pf_ctx* c, const double* u0, double tol, int k_max, const double* reference, double* states,
+                double* coarse_new, double* coarse_old, double* fine_endpoints, double* diffs,
+                double* iteration_times, double* errors, int* iterations, int* stop_reason) {
+  if (!c || !u0) return PF_ERR_ARGUMENT;
+  if (k_max < 1) return set_error(c, PF_ERR_ARGUMENT, "k_max must be at least 1");
+  const auto t0 = std::chrono::steady_clock::now();
+  const int nt = c->grid.nt;
+  const size_t sz = c->size;
+  int rc = pf_dev_parareal_init(c, u0);
+  if (rc) return rc;
+  std::vector<double> last(sz), tmp(sz);
+  if (reference && errors) {
+    if (download(c, last.data(), c->U.p + (size_t)nt * sz, sz)) return c->err.code;
+    PF_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < sz; ++i) tmp[i] = last[i] - reference[(size_t)nt * sz + i];
+    errors[0] = host_norm(c, tmp.data());
+  }
+  int iters = 0, stop = 0;
+  for (int k = 0; k < k_max; ++k) {
+    rc = pf_dev_fine_sweep(c, c->U.p, 0, nt, c->fold.p);
+    if (rc) return rc;
+    double diff = 0.0;
+    rc = pf_dev_parareal_correct(c, c->fold.p, k, &diff);
+    if (rc) return rc;
+    if (diffs) diffs[k] = diff;
+    if (iteration_times)
+      iteration_times[k] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (reference && errors) {
+      if (download(c, last.data(), c->U.p + (size_t)nt * sz, sz)) return c->err.code;
+      PF_CUDA(c, cudaStreamSynchronize(c->stream));
+      for (size_t i = 0; i < sz; ++i) tmp[i] = last[i] - reference[(size_t)nt * sz + i];
+      errors[k + 1] = host_norm(c, tmp.data());
+    }
+    iters = k + 1;
+    if (tol > 0 && diff < tol) {
+      stop = 1;
+      break;
+    }
+  }
+  if (fine_endpoints && download(c, fine_endpoints, c->fold.p, (size_t)nt * sz)) return c->err.code;
+  rc = pf_dev_parareal_read(c, states, coarse_new, coarse_old);
+  if (rc) return rc;
+  if (iterations) *iterations = iters;
+  if (stop_reason) *stop_reason = stop;
+  return 0;
+}
+
+}  // extern "C"

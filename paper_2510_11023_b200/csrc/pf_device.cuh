@@ -1,0 +1,145 @@
+// Device-side primitives shared by every space: complex arithmetic,
+// deterministic block reductions, coefficient functors, status words.
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace pf {
+
+struct cd {
+  double x, y;
+};
+__device__ __forceinline__ cd cmul(cd a, cd b) { return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
+__device__ __forceinline__ cd cmulc(cd a, cd b) {  // a * conj(b)
+  return {a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y};
+}
+__device__ __forceinline__ cd cadd(cd a, cd b) { return {a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ cd csub(cd a, cd b) { return {a.x - b.x, a.y - b.y}; }
+
+// ---------------------------------------------------------------------------
+// status: one word per CTA, decoded on the host into pf_error
+// ---------------------------------------------------------------------------
+enum StatusCode : int { ST_OK = 0, ST_SOLVER = 2, ST_COEFF = 3, ST_DIVERGE = 4 };
+
+struct Status {
+  int code;   // StatusCode
+  int n;      // slice / coarse step
+  int r;      // substep (-1 for coarse)
+  int node;   // coefficient node
+  int iters;  // PCG iterations accumulated by this CTA
+  int solves; // linear solves performed by this CTA
+  int pad[2];
+};
+
+// ---------------------------------------------------------------------------
+// coefficient functors (include/parafrac_b200.h PF_FN_*)
+// ---------------------------------------------------------------------------
+struct Fn {
+  int id;
+  double p[6];
+};
+
+__device__ __forceinline__ double fn_D(const Fn& f, double x, double x2, double t, double u) {
+  switch (f.id) {
+    case 1:  // PF_FN_POLY
+      return f.p[0] + f.p[1] * u;
+    case 2: {  // PF_FN_CFG12
+      const double u2 = u * u;
+      return 1.0 + u2 / (1.0 + u2);
+    }
+    case 3:  // PF_FN_CFG3
+      return 1.5 + 0.5 * tanh(u);
+    case 4: {  // PF_FN_CFG45
+      const double s = sin(u);
+      return (1.0 + 0.5 * x) * (1.0 + 0.5 * (s * s));
+    }
+    case 5:  // PF_FN_NAN_AT
+      return fabs(x - f.p[0]) < 1e-12 ? CUDART_NAN : f.p[1];
+    default:
+      return CUDART_NAN;
+  }
+}
+
+__device__ __forceinline__ double fn_f(const Fn& f, double x, double x2, double t, double u) {
+  switch (f.id) {
+    case 1:
+      return __dadd_rn(__dmul_rn(f.p[2], u), __dmul_rn(f.p[3], __dmul_rn(sin(CUDART_PI * x), exp(-t))));
+    case 2:
+      return sin(CUDART_PI * x) * cos(u);
+    case 3:
+      return -u + 0.1 * sin(2.0 * CUDART_PI * x);
+    case 4: {
+      const double u2 = u * u;
+      return u * (1.0 - u2) / (1.0 + u2);
+    }
+    default:
+      return 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// deterministic block reductions (fixed order; every thread gets the total)
+// `red` holds 2 buffers x 32 warps x 2 values.  One __syncthreads each.
+// ---------------------------------------------------------------------------
+template <int NT>
+struct Reducer {
+  double* red;
+  int buf;
+  __device__ void init(double* scratch) {
+    red = scratch;
+    buf = 0;
+  }
+  __device__ __forceinline__ double2 sum2(double a, double b) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    const int w = threadIdx.x >> 5;
+    double* slot = red + buf * 64;
+    if ((threadIdx.x & 31) == 0) {
+      slot[2 * w] = a;
+      slot[2 * w + 1] = b;
+    }
+    __syncthreads();
+    double sa = 0.0, sb = 0.0;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) {
+      sa += slot[2 * i];
+      sb += slot[2 * i + 1];
+    }
+    buf ^= 1;
+    return make_double2(sa, sb);
+  }
+  __device__ __forceinline__ double sum(double a) { return sum2(a, 0.0).x; }
+  __device__ __forceinline__ double max(double a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    const int w = threadIdx.x >> 5;
+    double* slot = red + buf * 64;
+    if ((threadIdx.x & 31) == 0) slot[2 * w] = a;
+    __syncthreads();
+    double s = slot[0];
+#pragma unroll
+    for (int i = 1; i < NT / 32; ++i) s = fmax(s, slot[2 * i]);
+    buf ^= 1;
+    return s;
+  }
+  // smallest integer over the block (error indices); INT_MAX = none
+  __device__ __forceinline__ int min_int(int a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+    const int w = threadIdx.x >> 5;
+    double* slot = red + buf * 64;
+    if ((threadIdx.x & 31) == 0) slot[2 * w] = (double)a;
+    __syncthreads();
+    double s = slot[0];
+#pragma unroll
+    for (int i = 1; i < NT / 32; ++i) s = fmin(s, slot[2 * i]);
+    buf ^= 1;
+    return (int)s;
+  }
+};
+
+}  // namespace pf

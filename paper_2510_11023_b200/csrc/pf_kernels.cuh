@@ -1,0 +1,418 @@
+// Kernels templated over a space (Sine1D / Cheb1D):
+//
+//   k_fine_sweep   one CTA per slice, persistent over all m substeps
+//                  (stepping.fine_sweep_intervals, stepping.py:189-243)
+//   k_coarse       one CTA; run_coarse / the parareal correction sweep with
+//                  guards and diff / a single coarse step
+//                  (stepping.py:87-121, parareal.py:114-128)
+//   k_sequential   one CTA; the full-history fine solver (stepping.py:260-288)
+//
+// Thread ownership of state entries is e = threadIdx.x + i*NT (i < EPT) in
+// every kernel, so a thread only ever re-reads history rows it wrote itself.
+#pragma once
+#include "pf_device.cuh"
+
+namespace pf {
+
+struct Common {
+  Fn fn;
+  int size;  // state entries
+  int nt, m;
+  double dT, dt, gam_f, gam_c, minv;  // minv = m^-alpha
+  const double* bfine;                // b_q
+  const double* afine;                // a_s = b_{s-1} - b_s (s >= 1; a_0 unused)
+  const double* bfrac;                // b_{q/m}
+  double* scratch;                    // per-slice block history / bracket rows
+};
+
+// Block length of the blocked L1 history: each history row is read once per
+// HB substeps and reused for HB target rows (register-tiled Toeplitz GEMM).
+constexpr int HB = 16;
+
+// Far history for the HB target rows r = R0+1 .. R0+HB of one slice
+// (the einsum of stepping.py:234 restricted to j <= R0):
+//   out[rr] = b_{R0+rr} path[0] + sum_{j=1}^{R0} a_{R0+1+rr-j} path[j]
+// Weights are Toeplitz in (r, j): a J-row chunk needs HB+J-1 of them.
+template <int NT, int EPT, int J>
+__device__ __forceinline__ void far_history_block(const Common& c, const double* path, int R0, double* out) {
+  double acc[HB][EPT];
+  double c0[EPT];
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int e = threadIdx.x + i * NT;
+    c0[i] = (e < c.size) ? path[e] : 0.0;
+  }
+#pragma unroll
+  for (int rr = 0; rr < HB; ++rr) {
+    const double w = c.bfine[R0 + rr];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) acc[rr][i] = w * c0[i];
+  }
+  for (int j0 = 1; j0 <= R0; j0 += J) {
+    double cv[J][EPT];
+#pragma unroll
+    for (int t = 0; t < J; ++t) {
+      const double* row = path + (size_t)(j0 + t) * c.size;
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        const int e = threadIdx.x + i * NT;
+        cv[t][i] = (e < c.size && j0 + t <= R0) ? row[e] : 0.0;
+      }
+    }
+    // wv[u] = a_{R0+1-j0-(J-1)+u}, u = rr - t + J - 1
+    double wv[HB + J - 1];
+    const int s0 = R0 + 1 - j0 - (J - 1);
+#pragma unroll
+    for (int u = 0; u < HB + J - 1; ++u) {
+      const int s = s0 + u;
+      wv[u] = c.afine[s < 1 ? 1 : s];
+    }
+#pragma unroll
+    for (int t = 0; t < J; ++t)
+#pragma unroll
+      for (int rr = 0; rr < HB; ++rr)
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) acc[rr][i] = fma(wv[rr - t + J - 1], cv[t][i], acc[rr][i]);
+  }
+#pragma unroll
+  for (int rr = 0; rr < HB; ++rr)
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = threadIdx.x + i * NT;
+      if (e < c.size) out[(size_t)rr * c.size + e] = acc[rr][i];
+    }
+}
+
+// Coarse-history bracket rows for r = r0 .. r0+HB-1 of slice n
+// (stepping.py:124-139): -m^-alpha sum_{j<n} b_{j + r/m} (U_{n-j} - U_{n-j-1}).
+template <int NT, int EPT>
+__device__ __forceinline__ void bracket_block(const Common& c, const double* __restrict__ U, int n, int r0,
+                                              double* out) {
+  double acc[HB][EPT];
+#pragma unroll
+  for (int rr = 0; rr < HB; ++rr)
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) acc[rr][i] = 0.0;
+  for (int j = 0; j < n; ++j) {
+    double inc[EPT];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = threadIdx.x + i * NT;
+      inc[i] = (e < c.size) ? U[(size_t)(n - j) * c.size + e] - U[(size_t)(n - j - 1) * c.size + e] : 0.0;
+    }
+    const double* w = c.bfrac + (size_t)j * c.m + r0;
+#pragma unroll
+    for (int rr = 0; rr < HB; ++rr) {
+      const double wr = w[rr];
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) acc[rr][i] = fma(wr, inc[i], acc[rr][i]);
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < HB; ++rr)
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = threadIdx.x + i * NT;
+      if (e < c.size) out[(size_t)rr * c.size + e] = (n > 0) ? -c.minv * acc[rr][i] : 0.0;
+    }
+}
+
+// L1 history of one slice at substep r (einsum at stepping.py:234):
+//   h = b_{r-1} path[0] + sum_{j=1}^{r-1} (b_{r-j-1} - b_{r-j}) path[j]
+template <int NT, int EPT>
+__device__ __forceinline__ void history_sum(const Common& c, const double* path, int r,
+                                            double* h) {
+  const double* __restrict__ b = c.bfine;
+  const double b0 = b[r - 1];
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int e = threadIdx.x + i * NT;
+    h[i] = (e < c.size) ? b0 * path[e] : 0.0;
+  }
+  int j = 1;
+  for (; j + 3 < r; j += 4) {
+    const double w0 = b[r - j - 1] - b[r - j];
+    const double w1 = b[r - j - 2] - b[r - j - 1];
+    const double w2 = b[r - j - 3] - b[r - j - 2];
+    const double w3 = b[r - j - 4] - b[r - j - 3];
+    const double* p0 = path + (size_t)j * c.size;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = threadIdx.x + i * NT;
+      if (e < c.size) {
+        const double v0 = p0[e], v1 = p0[c.size + e], v2 = p0[2 * c.size + e], v3 = p0[3 * c.size + e];
+        double acc = fma(w0, v0, h[i]);
+        acc = fma(w1, v1, acc);
+        acc = fma(w2, v2, acc);
+        h[i] = fma(w3, v3, acc);
+      }
+    }
+  }
+  for (; j < r; ++j) {
+    const double w = b[r - j - 1] - b[r - j];
+    const double* p0 = path + (size_t)j * c.size;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = threadIdx.x + i * NT;
+      if (e < c.size) h[i] = fma(w, p0[e], h[i]);
+    }
+  }
+}
+
+// coarse-history bracket of slice n for target (n, r)  (stepping.py:124-139):
+//   -m^-alpha sum_{j=0}^{n-1} b_{j + r/m} (U_{n-j} - U_{n-j-1})
+template <int NT, int EPT>
+__device__ __forceinline__ void coarse_bracket(const Common& c, const double* __restrict__ U, int n, int r,
+                                               double* ct) {
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int e = threadIdx.x + i * NT;
+    double s = 0.0;
+    if (e < c.size && n > 0) {
+      for (int j = 0; j < n; ++j) {
+        const double inc = U[(size_t)(n - j) * c.size + e] - U[(size_t)(n - j - 1) * c.size + e];
+        s = fma(c.bfrac[(size_t)j * c.m + r], inc, s);
+      }
+      s = -c.minv * s;
+    }
+    ct[i] = s;
+  }
+}
+
+template <class SP, class SPP, int NT, int EPT>
+__global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const double* __restrict__ U, int n_lo,
+                                                   double* paths, double* __restrict__ out,
+                                                   Status* __restrict__ status) {
+  extern __shared__ __align__(16) char smem[];
+  SP sp;
+  sp.init(smem, spp);
+  const int b = blockIdx.x;
+  const int n = n_lo + b;
+  double* path = paths + (size_t)b * (c.m + 1) * c.size;
+  Status st = {ST_OK, n, 0, -1, 0, 0, {0, 0}};
+  double x[EPT];
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int e = threadIdx.x + i * NT;
+    x[i] = (e < c.size) ? U[(size_t)n * c.size + e] : 0.0;
+    if (e < c.size) path[e] = x[i];
+  }
+  double* hscr = c.scratch + (size_t)b * 2 * HB * c.size;
+  double* cscr = hscr + (size_t)HB * c.size;
+  for (int r = 1; r <= c.m; ++r) {
+    const double t = (double)n * c.dT + (double)(r - 1) * c.dt;
+    const int rr = (r - 1) % HB;
+    const int R0 = r - 1 - rr;
+    if (rr == 0) {
+      far_history_block<NT, EPT, (EPT > 2 ? 4 : 8)>(c, path, R0, hscr);
+      bracket_block<NT, EPT>(c, U, n, r, cscr);
+    }
+    double h[EPT], ct[EPT], xn[EPT];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = threadIdx.x + i * NT;
+      double acc = 0.0, cb = 0.0;
+      if (e < c.size) {
+        acc = hscr[(size_t)rr * c.size + e];
+        for (int j = R0 + 1; j < r; ++j) acc = fma(c.afine[r - j], path[(size_t)j * c.size + e], acc);
+        cb = cscr[(size_t)rr * c.size + e];
+      }
+      h[i] = acc;
+      ct[i] = cb;
+    }
+    const int code = sp.step(c.fn, x, t, c.gam_f, h, ct, xn, st);
+    if (code != ST_OK) {
+      st.code = code;
+      st.r = r;
+      break;
+    }
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = threadIdx.x + i * NT;
+      x[i] = xn[i];
+      if (e < c.size) path[(size_t)r * c.size + e] = x[i];
+    }
+  }
+  if (st.code == ST_OK) {
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = threadIdx.x + i * NT;
+      if (e < c.size) out[(size_t)b * c.size + e] = x[i];
+    }
+  }
+  if (threadIdx.x == 0) status[b] = st;
+}
+
+// coarse step G(H[0..n]) -> x  (stepping.py:87-112)
+template <class SP, int NT, int EPT>
+__device__ __forceinline__ int coarse_apply(SP& sp, const Common& c, const double* H, int n, double* xout,
+                                            Status& st) {
+  double h[EPT], z[EPT], xp[EPT];
+  const double* __restrict__ b = c.bfine;
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int e = threadIdx.x + i * NT;
+    z[i] = 0.0;
+    h[i] = 0.0;
+    xp[i] = 0.0;
+    if (e < c.size) {
+      double acc = b[n] * H[e];
+      for (int j = 1; j <= n; ++j) acc = fma(b[n - j] - b[n - j + 1], H[(size_t)j * c.size + e], acc);
+      h[i] = acc;
+      xp[i] = H[(size_t)n * c.size + e];
+    }
+  }
+  return sp.step(c.fn, xp, (double)n * c.dT, c.gam_c, h, z, xout, st);
+}
+
+enum CoarseMode : int { CM_RUN = 0, CM_CORRECT = 1, CM_SINGLE = 2 };
+
+struct CoarseArgs {
+  int mode;
+  int n_single;      // CM_SINGLE: history rows 0..n_single in `traj`
+  int k_iter;        // CM_CORRECT: iteration index for DivergenceError
+  double guard;      // CM_CORRECT: divergence guard
+  double* traj;      // CM_RUN: (nt+1) rows, row 0 preset; CM_SINGLE: history
+  const double* ucur;
+  const double* fold;
+  const double* gold;
+  double* gnew;
+  double* unext;
+  double* out;       // CM_SINGLE result; CM_CORRECT: out[0] = diff
+};
+
+template <class SP, class SPP, int NT, int EPT>
+__global__ void __launch_bounds__(NT) k_coarse(Common c, SPP spp, CoarseArgs a, Status* __restrict__ status) {
+  extern __shared__ __align__(16) char smem[];
+  SP sp;
+  sp.init(smem, spp);
+  Status st = {ST_OK, 0, -1, -1, 0, 0, {0, 0}};
+  double x[EPT];
+  if (a.mode == CM_SINGLE) {
+    st.n = a.n_single;
+    const int code = coarse_apply<SP, NT, EPT>(sp, c, a.traj, a.n_single, x, st);
+    if (code != ST_OK) {
+      st.code = code;
+    } else {
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        const int e = threadIdx.x + i * NT;
+        if (e < c.size) a.out[e] = x[i];
+      }
+    }
+  } else if (a.mode == CM_RUN) {
+    for (int n = 0; n < c.nt; ++n) {
+      st.n = n;
+      const int code = coarse_apply<SP, NT, EPT>(sp, c, a.traj, n, x, st);
+      if (code != ST_OK) {
+        st.code = code;
+        break;
+      }
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        const int e = threadIdx.x + i * NT;
+        if (e < c.size) a.traj[(size_t)(n + 1) * c.size + e] = x[i];
+      }
+    }
+  } else {  // CM_CORRECT (parareal.py:114-128)
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = threadIdx.x + i * NT;
+      if (e < c.size) a.unext[e] = a.ucur[e];
+    }
+    for (int n = 0; n < c.nt; ++n) {
+      st.n = n;
+      const int code = coarse_apply<SP, NT, EPT>(sp, c, a.unext, n, x, st);
+      if (code != ST_OK) {
+        st.code = code;
+        break;
+      }
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        const int e = threadIdx.x + i * NT;
+        if (e < c.size) {
+          const size_t o = (size_t)n * c.size + e;
+          a.gnew[o] = x[i];
+          a.unext[o + c.size] = a.fold[o] + (x[i] - a.gold[o]);
+        }
+      }
+    }
+    if (st.code == ST_OK) {
+      // guards and diff (parareal.py:120-128): same ownership, no sync needed
+      int first_bad = 0x7fffffff;
+      double nmax = -1.0, dmax = 0.0;
+      int nmax_at = 0;
+      for (int n = 0; n <= c.nt; ++n) {
+        double v[EPT], d[EPT];
+        int fin = 1;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+          const int e = threadIdx.x + i * NT;
+          v[i] = d[i] = 0.0;
+          if (e < c.size) {
+            v[i] = a.unext[(size_t)n * c.size + e];
+            d[i] = v[i] - a.ucur[(size_t)n * c.size + e];
+            if (!isfinite(v[i])) fin = 0;
+          }
+        }
+        const double2 s = sp.red.sum2(sp.norm2_partial(v), sp.norm2_partial(d));
+        const int allfin = sp.red.min_int(fin);
+        if (!allfin && first_bad == 0x7fffffff) first_bad = n;
+        const double nn = sqrt(s.x), dd = sqrt(s.y);
+        if (nn > nmax) {
+          nmax = nn;
+          nmax_at = n;
+        }
+        dmax = fmax(dmax, dd);
+      }
+      if (first_bad != 0x7fffffff) {
+        st.code = ST_DIVERGE;
+        st.n = first_bad;
+        st.r = 0;
+      } else if (nmax > a.guard) {
+        st.code = ST_DIVERGE;
+        st.n = nmax_at;
+        st.r = 1;
+      }
+      if (threadIdx.x == 0) a.out[0] = dmax;
+    }
+  }
+  if (threadIdx.x == 0) status[0] = st;
+}
+
+// full-history fine solver (stepping.py:260-288); hist has (total+1) rows
+template <class SP, class SPP, int NT, int EPT>
+__global__ void __launch_bounds__(NT) k_sequential(Common c, SPP spp, double* hist, int total,
+                                                   Status* __restrict__ status) {
+  extern __shared__ __align__(16) char smem[];
+  SP sp;
+  sp.init(smem, spp);
+  Status st = {ST_OK, 0, -1, -1, 0, 0, {0, 0}};
+  double x[EPT];
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int e = threadIdx.x + i * NT;
+    x[i] = (e < c.size) ? hist[e] : 0.0;
+  }
+  for (int jj = 1; jj <= total; ++jj) {
+    double h[EPT], z[EPT], xn[EPT];
+    history_sum<NT, EPT>(c, hist, jj, h);
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) z[i] = 0.0;
+    st.n = jj - 1;
+    const int code = sp.step(c.fn, x, (double)(jj - 1) * c.dt, c.gam_f, h, z, xn, st);
+    if (code != ST_OK) {
+      st.code = code;
+      break;
+    }
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = threadIdx.x + i * NT;
+      x[i] = xn[i];
+      if (e < c.size) hist[(size_t)jj * c.size + e] = x[i];
+    }
+  }
+  if (threadIdx.x == 0) status[0] = st;
+}
+
+}  // namespace pf
