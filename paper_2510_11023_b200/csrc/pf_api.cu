@@ -26,7 +26,9 @@ using pf::Status;
 
 namespace {
 
-enum Variant { V_NONE = 0, V_SINE_128_1, V_SINE_256_1, V_SINE_256_2, V_SINE_256_4, V_CHEB_128_1 };
+// Sine variants by log2(Q): (threads per CTA, modes per thread)
+//   LG 2-6: (32, 1)  LG 7: (32, 2)  LG 8: (64, 2)  LG 9: (128, 2)  LG 10: (256, 2)  LG 11: (256, 4)
+enum Variant { V_NONE = 0, V_S2, V_S3, V_S4, V_S5, V_S6, V_S7, V_S8, V_S9, V_S10, V_S11, V_CHEB_128_1 };
 
 struct DevBuf {
   double* p = nullptr;
@@ -64,7 +66,7 @@ struct pf_ctx {
   std::vector<double> h_bfine, h_bfrac, h_nodes, h_d1, h_qw;
   // device tables
   double *d_bfine = nullptr, *d_afine = nullptr, *d_bfrac = nullptr, *d_nodes = nullptr, *d_d1 = nullptr, *d_qw = nullptr;
-  cd *d_tw = nullptr, *d_ph = nullptr;
+  cd *d_tw = nullptr, *d_ph = nullptr;  // d_tw: per-pass twiddle tables
   long len_fine = 0, len_frac = 0;
   // work buffers
   DevBuf U, Unext, paths, fold, gold, gnew, io, scalar, scratch;
@@ -76,6 +78,7 @@ struct pf_ctx {
   pf_error err{};
   double guard = 0;
   bool parareal_ready = false;
+  int pending_lo = -1, pending_bs = 0;  // last async fine launch, decoded by pf_dev_check
 };
 
 namespace {
@@ -126,7 +129,7 @@ pf::Sine1DParams sine_params(const pf_ctx* c) {
   p.M = c->M;
   p.Q = c->Q;
   p.lgQ = c->lgQ;
-  p.tw = c->d_tw;
+  p.twp = c->d_tw;
   p.ph = c->d_ph;
   p.pcg_tol = c->pcg_tol;
   p.pcg_maxit = c->pcg_maxit;
@@ -144,44 +147,31 @@ pf::Cheb1DParams cheb_params(const pf_ctx* c) {
 }
 
 // Dispatch: binds SP (space type), SPP (its params), NT, EPT and `spp`.
-#define PF_DISPATCH(ctx, ...)                                        \
-  switch ((ctx)->variant) {                                          \
-    case V_SINE_128_1: {                                             \
-      using SP = pf::Sine1D<128, 1>;                                 \
-      using SPP = pf::Sine1DParams;                                  \
-      constexpr int NT = 128, EPT = 1;                               \
-      SPP spp = sine_params(ctx);                                    \
-      __VA_ARGS__;                                                   \
-    } break;                                                         \
-    case V_SINE_256_1: {                                             \
-      using SP = pf::Sine1D<256, 1>;                                 \
-      using SPP = pf::Sine1DParams;                                  \
-      constexpr int NT = 256, EPT = 1;                               \
-      SPP spp = sine_params(ctx);                                    \
-      __VA_ARGS__;                                                   \
-    } break;                                                         \
-    case V_SINE_256_2: {                                             \
-      using SP = pf::Sine1D<256, 2>;                                 \
-      using SPP = pf::Sine1DParams;                                  \
-      constexpr int NT = 256, EPT = 2;                               \
-      SPP spp = sine_params(ctx);                                    \
-      __VA_ARGS__;                                                   \
-    } break;                                                         \
-    case V_SINE_256_4: {                                             \
-      using SP = pf::Sine1D<256, 4>;                                 \
-      using SPP = pf::Sine1DParams;                                  \
-      constexpr int NT = 256, EPT = 4;                               \
-      SPP spp = sine_params(ctx);                                    \
-      __VA_ARGS__;                                                   \
-    } break;                                                         \
-    case V_CHEB_128_1: {                                             \
-      using SP = pf::Cheb1D<128, 1>;                                 \
-      using SPP = pf::Cheb1DParams;                                  \
-      constexpr int NT = 128, EPT = 1;                               \
-      SPP spp = cheb_params(ctx);                                    \
-      __VA_ARGS__;                                                   \
-    } break;                                                         \
-    default:                                                         \
+#define PF_DISPATCH(ctx, ...) \
+  switch ((ctx)->variant) { \
+    case V_S2: { using SP = pf::Sine1D<32, 1, 2>; using SPP = pf::Sine1DParams; \
+      constexpr int NT = 32, EPT = 1; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
+    case V_S3: { using SP = pf::Sine1D<32, 1, 3>; using SPP = pf::Sine1DParams; \
+      constexpr int NT = 32, EPT = 1; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
+    case V_S4: { using SP = pf::Sine1D<32, 1, 4>; using SPP = pf::Sine1DParams; \
+      constexpr int NT = 32, EPT = 1; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
+    case V_S5: { using SP = pf::Sine1D<32, 1, 5>; using SPP = pf::Sine1DParams; \
+      constexpr int NT = 32, EPT = 1; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
+    case V_S6: { using SP = pf::Sine1D<32, 1, 6>; using SPP = pf::Sine1DParams; \
+      constexpr int NT = 32, EPT = 1; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
+    case V_S7: { using SP = pf::Sine1D<32, 2, 7>; using SPP = pf::Sine1DParams; \
+      constexpr int NT = 32, EPT = 2; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
+    case V_S8: { using SP = pf::Sine1D<64, 2, 8>; using SPP = pf::Sine1DParams; \
+      constexpr int NT = 64, EPT = 2; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
+    case V_S9: { using SP = pf::Sine1D<128, 2, 9>; using SPP = pf::Sine1DParams; \
+      constexpr int NT = 128, EPT = 2; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
+    case V_S10: { using SP = pf::Sine1D<256, 2, 10>; using SPP = pf::Sine1DParams; \
+      constexpr int NT = 256, EPT = 2; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
+    case V_S11: { using SP = pf::Sine1D<256, 4, 11>; using SPP = pf::Sine1DParams; \
+      constexpr int NT = 256, EPT = 4; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
+    case V_CHEB_128_1: { using SP = pf::Cheb1D<128, 1>; using SPP = pf::Cheb1DParams; \
+      constexpr int NT = 128, EPT = 1; SPP spp = cheb_params(ctx); __VA_ARGS__; } break; \
+    default: \
       return set_error(ctx, PF_ERR_UNSUPPORTED, "no kernel variant"); \
   }
 
@@ -341,14 +331,16 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
   c->pcg_maxit = space->pcg_maxit > 0 ? space->pcg_maxit : 500;
   if (space->kind == PF_SPACE_SINE1D) {
     const int M = space->modes;
-    if (!is_pow2(M) || M > 1024) return set_error(c, PF_ERR_UNSUPPORTED, "sine modes must be a power of two <= 1024");
+    if (!is_pow2(M) || M < 2 || M > 1024)
+      return set_error(c, PF_ERR_UNSUPPORTED, "sine modes must be a power of two in [2, 1024]");
     c->M = M;
     c->Q = 2 * M;
     c->lgQ = 0;
     while ((1 << c->lgQ) < c->Q) ++c->lgQ;
     c->size = M;
-    c->variant = M <= 128 ? V_SINE_128_1 : M <= 256 ? V_SINE_256_1 : M <= 512 ? V_SINE_256_2 : V_SINE_256_4;
-    c->smem = pf::Sine1D<256, 1>::smem_bytes(M);
+    static const Variant by_lg[12] = {V_NONE, V_NONE, V_S2, V_S3, V_S4, V_S5, V_S6, V_S7, V_S8, V_S9, V_S10, V_S11};
+    c->variant = by_lg[c->lgQ];
+    c->smem = sizeof(cd) * (pf::tw_table_size(c->lgQ) + 3 * c->Q) + sizeof(double) * (c->Q + 128);
   } else if (space->kind == PF_SPACE_CHEB1D) {
     const int deg = space->modes;
     if (deg < 2) return set_error(c, PF_ERR_ARGUMENT, "degree must be at least 2 so interior nodes exist");
@@ -411,17 +403,33 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
   PF_CUDA(c, cudaMemcpy(c->d_afine, h_afine.data(), sizeof(double) * h_afine.size(), cudaMemcpyHostToDevice));
   PF_CUDA(c, cudaMemcpy(c->d_bfrac, c->h_bfrac.data(), sizeof(double) * need_frac, cudaMemcpyHostToDevice));
   if (c->kind == PF_SPACE_SINE1D) {
-    std::vector<cd> tw(c->Q), ph(c->Q);
+    const int ntw = std::max(pf::tw_table_size(c->lgQ), 1);
+    std::vector<cd> tw(ntw), ph(c->Q);
     const long double PI = 3.141592653589793238462643383279502884L;
+    // per-pass radix-4 twiddles w_r(k) = exp(-2 pi i r k / (4 Ns)), then radix-2 exp(-2 pi i k / (2 Ns))
+    int off = 0;
+    for (int p = 1, ns = 4; p < c->lgQ / 2; ++p, ns *= 4) {
+      for (int r = 1; r <= 3; ++r)
+        for (int k = 0; k < ns; ++k) {
+          const long double a = -2.0L * PI * (long double)(r * k) / (4.0L * ns);
+          tw[off + (r - 1) * ns + k] = {(double)cosl(a), (double)sinl(a)};
+        }
+      off += 3 * ns;
+    }
+    if (c->lgQ & 1) {
+      const int ns = 1 << (c->lgQ - 1);
+      for (int k = 0; k < ns; ++k) {
+        const long double a = -2.0L * PI * (long double)k / (2.0L * ns);
+        tw[off + k] = {(double)cosl(a), (double)sinl(a)};
+      }
+    }
     for (int j = 0; j < c->Q; ++j) {
-      const long double a = -2.0L * PI * (long double)j / (long double)c->Q;
-      tw[j] = {(double)cosl(a), (double)sinl(a)};
       const long double b = PI * (long double)j / (2.0L * (long double)c->Q);
       ph[j] = {(double)cosl(b), (double)sinl(b)};
     }
-    PF_CUDA(c, cudaMalloc(&c->d_tw, sizeof(cd) * c->Q));
+    PF_CUDA(c, cudaMalloc(&c->d_tw, sizeof(cd) * ntw));
     PF_CUDA(c, cudaMalloc(&c->d_ph, sizeof(cd) * c->Q));
-    PF_CUDA(c, cudaMemcpy(c->d_tw, tw.data(), sizeof(cd) * c->Q, cudaMemcpyHostToDevice));
+    PF_CUDA(c, cudaMemcpy(c->d_tw, tw.data(), sizeof(cd) * ntw, cudaMemcpyHostToDevice));
     PF_CUDA(c, cudaMemcpy(c->d_ph, ph.data(), sizeof(cd) * c->Q, cudaMemcpyHostToDevice));
   } else {
     PF_CUDA(c, cudaMalloc(&c->d_nodes, sizeof(double) * c->npts));
@@ -481,18 +489,27 @@ int pf_dev_fine_sweep_async(pf_ctx* c, const double* d_u, int n_lo, int n_hi, do
   if (bs < 1 || n_lo < 0 || n_hi > c->grid.nt) return set_error(c, PF_ERR_ARGUMENT, "interval range outside the supplied coarse states");
   cudaSetDevice(c->device);
   if (ensure_status(c, bs)) return c->err.code;
+  c->pending_lo = n_lo;
+  c->pending_bs = bs;
   return launch_fine(c, d_u, n_lo, bs, d_out, c->d_status);
 }
 
 int pf_dev_fine_sweep(pf_ctx* c, const double* d_u, int n_lo, int n_hi, double* d_out) {
   int rc = pf_dev_fine_sweep_async(c, d_u, n_lo, n_hi, d_out);
   if (rc) return rc;
+  c->pending_lo = -1;
   return decode_fine(c, n_lo, n_hi - n_lo);
 }
 
+// Synchronise; decode the status of the last asynchronous fine launch.
 int pf_dev_check(pf_ctx* c) {
   if (!c) return PF_ERR_ARGUMENT;
   PF_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (c->pending_lo >= 0) {
+    const int lo = c->pending_lo, bs = c->pending_bs;
+    c->pending_lo = -1;
+    return decode_fine(c, lo, bs);
+  }
   return 0;
 }
 

@@ -91,10 +91,15 @@ struct Reducer {
     buf = 0;
   }
   __device__ __forceinline__ double2 sum2(double a, double b) {
+    // xor butterfly: every lane ends with the bitwise-same sum (IEEE add commutes)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       a += __shfl_xor_sync(0xffffffffu, a, o);
       b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (NT == 32) {
+      __syncwarp();  // orders the warp's smem traffic like the block barrier does
+      return make_double2(a, b);
     }
     const int w = threadIdx.x >> 5;
     double* slot = red + buf * 64;
@@ -116,6 +121,10 @@ struct Reducer {
   __device__ __forceinline__ double max(double a) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (NT == 32) {
+      __syncwarp();
+      return a;
+    }
     const int w = threadIdx.x >> 5;
     double* slot = red + buf * 64;
     if ((threadIdx.x & 31) == 0) slot[2 * w] = a;
@@ -130,6 +139,10 @@ struct Reducer {
   __device__ __forceinline__ int min_int(int a) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (NT == 32) {
+      __syncwarp();
+      return a;
+    }
     const int w = threadIdx.x >> 5;
     double* slot = red + buf * 64;
     if ((threadIdx.x & 31) == 0) slot[2 * w] = (double)a;

@@ -16,6 +16,11 @@
 // (sin(pi(Q-j)(2q+1)/2Q) = (-1)^q cos(pi j(2q+1)/2Q)), and every DCT pair runs
 // as one length-Q complex Stockham FFT in shared memory (Makhoul's
 // even/odd reordering), so the dense S, S' (Q x M) are never formed.
+//
+// FFT layout: complex doubles at swizzled slots sw(i) = i ^ ((i>>2)&7), which
+// makes every radix-4 Stockham load/store pass bank-conflict free for
+// 16-byte elements (checked exhaustively for Q = 16..2048); twiddles come from
+// per-pass tables w_r(k) = exp(-2 pi i r k / (4 Ns)), independent of Q.
 #pragma once
 #include "pf_device.cuh"
 
@@ -23,72 +28,92 @@ namespace pf {
 
 struct Sine1DParams {
   int M, Q, lgQ;
-  const cd* tw;  // Q: exp(-2 pi i j / Q)
-  const cd* ph;  // Q: exp(+i pi j / (2Q))
+  const cd* twp;  // per-pass twiddle tables (see tw_table_size)
+  const cd* ph;   // Q: exp(+i pi j / (2Q))
   double pcg_tol;
   int pcg_maxit;
 };
 
-// ---------------------------------------------------------------------------
-// Stockham autosort FFT, radix 4 (+ one radix-2 pass for odd log2 L), in smem.
-// inv=false: X_k = sum x_n exp(-2 pi i kn/L); inv=true: exp(+...), unnormalised.
-// Returns the buffer that holds the result.  Ends with a __syncthreads.
-// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int tw_table_size(int lg) {
+  int n = 0, ns = 4;
+  for (int p = 1; p < lg / 2; ++p, ns *= 4) n += 3 * ns;
+  if (lg & 1) n += 1 << (lg - 1);
+  return n;
+}
+
+__device__ __forceinline__ int sw(int i) { return i ^ ((i >> 2) & 7); }
+
 template <int NT>
-__device__ __forceinline__ cd* fft_stockham(cd* a, cd* b, const cd* __restrict__ tw, int L, int lg,
-                                            bool inv) {
-  int Ns = 1;
-  const int L4 = L >> 2;
-  for (int pass = 0; pass < (lg >> 1); ++pass) {
-    const int step = L4 / Ns;
-    for (int j = threadIdx.x; j < L4; j += NT) {
-      const int k = j & (Ns - 1);
-      cd v0 = a[j], v1 = a[j + L4], v2 = a[j + 2 * L4], v3 = a[j + 3 * L4];
-      if (Ns > 1) {
-        const int i1 = k * step;
-        cd w1 = tw[i1], w2 = tw[2 * i1], w3 = tw[3 * i1];
-        if (inv) {
-          w1.y = -w1.y;
-          w2.y = -w2.y;
-          w3.y = -w3.y;
-        }
-        v1 = cmul(v1, w1);
-        v2 = cmul(v2, w2);
-        v3 = cmul(v3, w3);
-      }
-      const cd t0 = cadd(v0, v2), t1 = csub(v0, v2), t2 = cadd(v1, v3), t3 = csub(v1, v3);
-      // -i*t3 = (t3.y, -t3.x)
-      const cd mi3 = {t3.y, -t3.x};
-      const cd X0 = cadd(t0, t2), X2 = csub(t0, t2);
-      const cd Xa = cadd(t1, mi3), Xb = csub(t1, mi3);  // forward: X1 = Xa, X3 = Xb
-      const int base = ((j - k) << 2) + k;
-      b[base] = X0;
-      b[base + Ns] = inv ? Xb : Xa;
-      b[base + 2 * Ns] = X2;
-      b[base + 3 * Ns] = inv ? Xa : Xb;
-    }
+__device__ __forceinline__ void bar() {
+  if (NT == 32)
+    __syncwarp();
+  else
     __syncthreads();
+}
+
+// Stockham autosort FFT of length 2^LG on swizzled smem, radix 4 (+ a final
+// radix-2 pass for odd LG).  INV: exp(+2 pi i kn/L), unnormalised.
+// Returns the buffer holding the result; ends with a barrier.
+template <int LG, int NT, bool INV>
+__device__ __forceinline__ cd* fft_stockham(cd* a, cd* b, const cd* __restrict__ twp) {
+  constexpr int L = 1 << LG;
+  constexpr int L4 = L >> 2;
+  int off = 0;
+#pragma unroll
+  for (int pass = 0; pass < LG / 2; ++pass) {
+    const int Ns = 1 << (2 * pass);
+#pragma unroll
+    for (int j0 = 0; j0 < L4; j0 += NT) {
+      const int j = j0 + (int)threadIdx.x;
+      if (L4 % NT == 0 || j < L4) {
+        const int k = j & (Ns - 1);
+        cd v0 = a[sw(j)], v1 = a[sw(j + L4)], v2 = a[sw(j + 2 * L4)], v3 = a[sw(j + 3 * L4)];
+        if (pass > 0) {
+          cd w1 = twp[off + k], w2 = twp[off + Ns + k], w3 = twp[off + 2 * Ns + k];
+          if (INV) {
+            w1.y = -w1.y;
+            w2.y = -w2.y;
+            w3.y = -w3.y;
+          }
+          v1 = cmul(v1, w1);
+          v2 = cmul(v2, w2);
+          v3 = cmul(v3, w3);
+        }
+        const cd t0 = cadd(v0, v2), t1 = csub(v0, v2), t2 = cadd(v1, v3), t3 = csub(v1, v3);
+        const cd mi3 = {t3.y, -t3.x};  // -i * t3
+        const int base = ((j - k) << 2) + k;
+        b[sw(base)] = cadd(t0, t2);
+        b[sw(base + Ns)] = INV ? csub(t1, mi3) : cadd(t1, mi3);
+        b[sw(base + 2 * Ns)] = csub(t0, t2);
+        b[sw(base + 3 * Ns)] = INV ? cadd(t1, mi3) : csub(t1, mi3);
+      }
+    }
+    if (pass > 0) off += 3 * Ns;
+    bar<NT>();
     cd* t = a;
     a = b;
     b = t;
-    Ns <<= 2;
   }
-  if (lg & 1) {
-    const int L2 = L >> 1;
-    const int step = L2 / Ns;
-    for (int j = threadIdx.x; j < L2; j += NT) {
-      const int k = j & (Ns - 1);
-      cd v0 = a[j], v1 = a[j + L2];
-      if (Ns > 1) {
-        cd w = tw[k * step];
-        if (inv) w.y = -w.y;
-        v1 = cmul(v1, w);
+  if (LG & 1) {
+    constexpr int L2 = L >> 1;
+    constexpr int Ns = 1 << (LG - 1);
+#pragma unroll
+    for (int j0 = 0; j0 < L2; j0 += NT) {
+      const int j = j0 + (int)threadIdx.x;
+      if (L2 % NT == 0 || j < L2) {
+        const int k = j & (Ns - 1);
+        cd v0 = a[sw(j)], v1 = a[sw(j + L2)];
+        if (Ns > 1) {
+          cd w = twp[off + k];
+          if (INV) w.y = -w.y;
+          v1 = cmul(v1, w);
+        }
+        const int base = ((j - k) << 1) + k;
+        b[sw(base)] = cadd(v0, v1);
+        b[sw(base + Ns)] = csub(v0, v1);
       }
-      const int base = ((j - k) << 1) + k;
-      b[base] = cadd(v0, v1);
-      b[base + Ns] = csub(v0, v1);
     }
-    __syncthreads();
+    bar<NT>();
     cd* t = a;
     a = b;
     b = t;
@@ -96,45 +121,34 @@ __device__ __forceinline__ cd* fft_stockham(cd* a, cd* b, const cd* __restrict__
   return a;
 }
 
-template <int NT, int EPT>
+template <int NT, int EPT, int LG>
 struct Sine1D {
   static constexpr double SQ2 = 1.4142135623730951;
-  int M, Q, lgQ;
-  const cd* tw;
+  static constexpr int Q = 1 << LG;
+  static constexpr int M = Q / 2;
+  static constexpr int QPT = (Q + NT - 1) / NT;
+  static constexpr int TW = tw_table_size(LG);
+  const cd* twp;
   const cd* ph;
   cd *A, *B;
-  double *dq, *sa, *sb;
+  double* dq;
   Reducer<NT> red;
   double tol2;
   int maxit;
 
-  static size_t smem_bytes(int M) {
-    const size_t Q = 2 * (size_t)M;
-    return Q * sizeof(cd) * 4 + Q * sizeof(double) + 2 * (Q + 1) * sizeof(double) + 128 * sizeof(double);
-  }
+  static size_t smem_bytes() { return sizeof(cd) * (TW + 3 * Q) + sizeof(double) * (Q + 128); }
 
   __device__ void init(char* smem, const Sine1DParams& p) {
-    M = p.M;
-    Q = p.Q;
-    lgQ = p.lgQ;
     cd* s = reinterpret_cast<cd*>(smem);
     cd* tws = s;
-    cd* phs = s + Q;
-    A = s + 2 * Q;
-    B = s + 3 * Q;
-    dq = reinterpret_cast<double*>(s + 4 * Q);
-    sa = dq + Q;
-    sb = sa + (Q + 1);
-    red.init(sb + (Q + 1));
-    for (int j = threadIdx.x; j < Q; j += NT) {
-      tws[j] = p.tw[j];
-      phs[j] = p.ph[j];
-    }
-    for (int j = threadIdx.x; j <= Q; j += NT) {
-      sa[j] = 0.0;
-      sb[j] = 0.0;
-    }
-    tw = tws;
+    cd* phs = s + TW;
+    A = phs + Q;
+    B = A + Q;
+    dq = reinterpret_cast<double*>(B + Q);
+    red.init(dq + Q);
+    for (int j = threadIdx.x; j < TW; j += NT) tws[j] = p.twp[j];
+    for (int j = threadIdx.x; j < Q; j += NT) phs[j] = p.ph[j];
+    twp = tws;
     ph = phs;
     tol2 = p.pcg_tol * p.pcg_tol;
     maxit = p.pcg_maxit;
@@ -142,134 +156,147 @@ struct Sine1D {
   }
 
   __device__ __forceinline__ int mode(int i) const { return 1 + (int)threadIdx.x + i * NT; }
+  __device__ __forceinline__ static int perm(int q) { return (q & 1) ? (Q - 1 - (q >> 1)) : (q >> 1); }
 
-  // node index of grid point q in the Makhoul permutation
-  __device__ __forceinline__ int perm(int q) const { return (q & 1) ? (Q - 1 - (q >> 1)) : (q >> 1); }
-
-  // Euclidean norm^2 partial of owned coefficients (Parseval: = L2 norm of u)
-  __device__ __forceinline__ double wdot(const double* a, const double* b) const {
+  __device__ __forceinline__ double norm2_partial(const double* v) const {
     double s = 0.0;
 #pragma unroll
     for (int i = 0; i < EPT; ++i)
-      if (mode(i) <= M) s = fma(a[i], b[i], s);
-    return s;
-  }
-  __device__ double norm_partial_global(const double* v) const {
-    double s = 0.0;
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int e = threadIdx.x + i * NT;
-      if (e < M) s = fma(v[e], v[e], s);
-    }
+      if (mode(i) <= M) s = fma(v[i], v[i], s);
     return s;
   }
 
-  // K p for owned modes (p, Kp in registers).  Uses sb, A, B, dq.
+  // FFT input of a synthesis pair: sine coefficients a_k, cosine coefficients b_k.
+  // W_j = ph_j (a_{Q-j} - i a_j) + i ph_j (b_j - i b_{Q-j}); since a, b vanish
+  // above M, mode k alone determines W_k and W_{Q-k}.
+  __device__ __forceinline__ void synth_input(const double* av, const double* bv) {
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int k = mode(i);
+      if (k < M) {
+        const cd p = ph[k], pq = ph[Q - k];
+        // V1_k = -i p a, V2_k = p b  -> W_k = V1 + i V2
+        const double a = av[i], b = bv[i];
+        const cd v1 = {p.y * a, -p.x * a};
+        const cd v2 = {p.x * b, p.y * b};
+        A[sw(k)] = {v1.x - v2.y, v1.y + v2.x};
+        // j = Q-k: V1 = pq a, V2 = -i pq b
+        const cd u1 = {pq.x * a, pq.y * a};
+        const cd u2 = {pq.y * b, -pq.x * b};
+        A[sw(Q - k)] = {u1.x - u2.y, u1.y + u2.x};
+      } else if (k == M) {
+        const cd p = ph[M];
+        const double a = av[i], b = bv[i];
+        const cd v1 = {p.x * a + p.y * a, p.y * a - p.x * a};  // p (a - i a)
+        const cd v2 = {p.x * b + p.y * b, p.y * b - p.x * b};  // p (b - i b)
+        A[sw(M)] = {v1.x - v2.y, v1.y + v2.x};
+      }
+    }
+    if (threadIdx.x == 0) A[0] = {0.0, 0.0};
+  }
+
+  // K p for owned modes (p, Kp in registers)
   __device__ __forceinline__ void apply_k(const double* p, double* kp) {
+    double av[EPT], bv[EPT];
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
-      const int k = mode(i);
-      if (k <= M) sb[k] = SQ2 * CUDART_PI * (double)k * p[i];
+      av[i] = 0.0;
+      bv[i] = SQ2 * CUDART_PI * (double)mode(i) * p[i];
     }
-    __syncthreads();
-    for (int j = threadIdx.x; j < Q; j += NT) {
-      const double bj = sb[j], bQ = sb[Q - j];
-      const cd pj = ph[j];
-      // V2 = ph*(bj - i bQ); W = i*V2
-      const cd V2 = {pj.x * bj + pj.y * bQ, pj.y * bj - pj.x * bQ};
-      A[j] = {-V2.y, V2.x};
-    }
-    __syncthreads();
-    cd* R = fft_stockham<NT>(A, B, tw, Q, lgQ, true);
+    synth_input(av, bv);
+    bar<NT>();
+    cd* R = fft_stockham<LG, NT, true>(A, B, twp);
     cd* O = (R == A) ? B : A;
-    for (int q = threadIdx.x; q < Q; q += NT) {
-      const int idx = perm(q);
-      const double v = 0.5 * R[idx].y;
-      R[idx] = {0.0, dq[q] * v};
+#pragma unroll
+    for (int i = 0; i < QPT; ++i) {
+      const int q = threadIdx.x + i * NT;
+      if (Q % NT == 0 || q < Q) {
+        const int s = sw(perm(q));
+        R[s] = {0.0, dq[q] * (0.5 * R[s].y)};
+      }
     }
-    __syncthreads();
-    cd* Z = fft_stockham<NT>(R, O, tw, Q, lgQ, false);
+    bar<NT>();
+    cd* Z = fft_stockham<LG, NT, false>(R, O, twp);
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int k = mode(i);
+      kp[i] = 0.0;
       if (k <= M) {
-        const cd a = Z[k], b = Z[Q - k], c = ph[k];
+        const cd a = Z[sw(k)], b = Z[sw(Q - k)], c = ph[k];
         const double Dx = a.x - b.x, Dy = a.y + b.y;
-        const double X2 = 0.5 * (c.x * Dy - c.y * Dx);
-        kp[i] = SQ2 * CUDART_PI * (double)k * X2;
+        kp[i] = SQ2 * CUDART_PI * (double)k * (0.5 * (c.x * Dy - c.y * Dx));
       }
     }
   }
 
   // One semi-implicit substep.  xprev: owned coefficients of c_prev.
-  // Returns 0 on success, else ST_* with st.node / fail info set.
   __device__ int step(const Fn& fn, const double* xprev, double t, double gam, const double* hist,
                       const double* contrib, double* xout, Status& st) {
     // --- synthesis pair: u = S c, v0 = S' c -----------------------------
+    {
+      double av[EPT], bv[EPT];
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int k = mode(i);
-      if (k <= M) {
-        sa[k] = SQ2 * xprev[i];
-        sb[k] = SQ2 * CUDART_PI * (double)k * xprev[i];
+      for (int i = 0; i < EPT; ++i) {
+        av[i] = SQ2 * xprev[i];
+        bv[i] = SQ2 * CUDART_PI * (double)mode(i) * xprev[i];
       }
+      synth_input(av, bv);
     }
-    __syncthreads();
-    for (int j = threadIdx.x; j < Q; j += NT) {
-      const double aj = sa[j], aQ = sa[Q - j], bj = sb[j], bQ = sb[Q - j];
-      const cd pj = ph[j];
-      const cd V1 = {pj.x * aQ + pj.y * aj, pj.y * aQ - pj.x * aj};
-      const cd V2 = {pj.x * bj + pj.y * bQ, pj.y * bj - pj.x * bQ};
-      A[j] = {V1.x - V2.y, V1.y + V2.x};
-    }
-    __syncthreads();
-    cd* R = fft_stockham<NT>(A, B, tw, Q, lgQ, true);
+    bar<NT>();
+    cd* R = fft_stockham<LG, NT, true>(A, B, twp);
     cd* O = (R == A) ? B : A;
     // --- pointwise coefficients (fused epilogue) ------------------------
     const double wq = 1.0 / (double)Q;
-    double dsum = 0.0;
+    double dsum = 0.0, nbad = 0.0;
     int bad = 0x7fffffff;
-    for (int q = threadIdx.x; q < Q; q += NT) {
-      const int idx = perm(q);
-      const cd w = R[idx];
-      const double s1 = 0.5 * w.x, s2 = 0.5 * w.y;
-      const double u = (q & 1) ? -s1 : s1;
-      const double xq = ((double)q + 0.5) / (double)Q;
-      const double Dv = fn_D(fn, xq, 0.0, t, u);
-      if (!isfinite(Dv)) bad = min(bad, q);
-      const double d = wq * Dv;
-      const double g = wq * fn_f(fn, xq, 0.0, t, u);
-      dq[q] = d;
-      dsum += d;
-      R[idx] = {(q & 1) ? -g : g, d * s2};
+#pragma unroll
+    for (int i = 0; i < QPT; ++i) {
+      const int q = threadIdx.x + i * NT;
+      if (Q % NT == 0 || q < Q) {
+        const int s = sw(perm(q));
+        const cd w = R[s];
+        const double s1 = 0.5 * w.x, s2 = 0.5 * w.y;
+        const double u = (q & 1) ? -s1 : s1;
+        const double xq = ((double)q + 0.5) / (double)Q;
+        const double Dv = fn_D(fn, xq, 0.0, t, u);
+        if (!isfinite(Dv)) {
+          bad = min(bad, q);
+          nbad += 1.0;
+        }
+        const double d = wq * Dv;
+        const double g = wq * fn_f(fn, xq, 0.0, t, u);
+        dq[q] = d;
+        dsum += d;
+        R[s] = {(q & 1) ? -g : g, d * s2};
+      }
     }
-    const int badq = red.min_int(bad);  // syncs
-    if (badq != 0x7fffffff) {
-      st.node = badq;
+    const double2 s01 = red.sum2(dsum, nbad);
+    if (s01.y > 0.0) {
+      st.node = red.min_int(bad);
       return ST_COEFF;
     }
-    const double dbar = red.sum(dsum);
+    const double dbar = s01.x;
     // --- analysis pair: F = S^T g, K c_prev = S'^T (d v0) ----------------
-    cd* Z = fft_stockham<NT>(R, O, tw, Q, lgQ, false);
-    double x[EPT], r[EPT], p[EPT], z[EPT], pinv[EPT], rhs[EPT];
+    cd* Z = fft_stockham<LG, NT, false>(R, O, twp);
+    double x[EPT], r[EPT], p[EPT], z[EPT], pinv[EPT];
     double bb = 0.0, rr = 0.0;
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int k = mode(i);
-      x[i] = r[i] = p[i] = z[i] = pinv[i] = rhs[i] = 0.0;
+      x[i] = r[i] = p[i] = z[i] = pinv[i] = 0.0;
       if (k <= M) {
-        const cd a = Z[k], b = Z[Q - k], c = ph[k], c2 = ph[Q - k];
+        const cd a = Z[sw(k)], b = Z[sw(Q - k)], c = ph[k], c2 = ph[Q - k];
         const double Dx = a.x - b.x, Dy = a.y + b.y;
         const double X2 = 0.5 * (c.x * Dy - c.y * Dx);
         const double X1 = 0.5 * (c2.x * (b.x + a.x) + c2.y * (b.y - a.y));
         const double F = SQ2 * X1;
         const double kx = SQ2 * CUDART_PI * (double)k * X2;
-        rhs[i] = __dadd_rn(__dadd_rn(hist[i], __dmul_rn(gam, F)), contrib[i]);
+        const double rhs = __dadd_rn(__dadd_rn(hist[i], __dmul_rn(gam, F)), contrib[i]);
         x[i] = xprev[i];
-        r[i] = rhs[i] - (x[i] + gam * kx);
+        r[i] = rhs - (x[i] + gam * kx);
         const double kk = (double)k;
         pinv[i] = 1.0 / (1.0 + gam * dbar * (CUDART_PI * CUDART_PI) * (kk * kk));
-        bb = fma(rhs[i], rhs[i], bb);
+        bb = fma(rhs, rhs, bb);
         rr = fma(r[i], r[i], rr);
       }
     }
@@ -299,20 +326,18 @@ struct Sine1D {
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
           qv[i] = p[i] + gam * kp[i];
-          pql = (mode(i) <= M) ? fma(p[i], qv[i], pql) : pql;
+          pql = fma(p[i], qv[i], pql);
         }
         const double pq = red.sum(pql);
         const double alpha = rz / pq;
         double rrl = 0.0, rzn = 0.0;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
-          if (mode(i) <= M) {
-            x[i] = fma(alpha, p[i], x[i]);
-            r[i] = fma(-alpha, qv[i], r[i]);
-            z[i] = pinv[i] * r[i];
-            rrl = fma(r[i], r[i], rrl);
-            rzn = fma(r[i], z[i], rzn);
-          }
+          x[i] = fma(alpha, p[i], x[i]);
+          r[i] = fma(-alpha, qv[i], r[i]);
+          z[i] = pinv[i] * r[i];
+          rrl = fma(r[i], r[i], rrl);
+          rzn = fma(r[i], z[i], rzn);
         }
         const double2 s = red.sum2(rrl, rzn);
         rrv = s.x;
@@ -325,18 +350,15 @@ struct Sine1D {
       st.iters += (it > maxit) ? maxit : it;
       if (it > maxit) return ST_SOLVER;
     }
-    int finite = 1;
+    double nonfinite = 0.0;
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
-      if (mode(i) <= M && !isfinite(x[i])) finite = 0;
+      if (mode(i) <= M && !isfinite(x[i])) nonfinite = 1.0;
       xout[i] = x[i];
     }
-    if (red.min_int(finite) == 0) return ST_SOLVER;
+    if (red.sum(nonfinite) > 0.0) return ST_SOLVER;
     return ST_OK;
   }
-
-  // norm^2 of owned values
-  __device__ __forceinline__ double norm2_partial(const double* v) const { return wdot(v, v); }
 };
 
 }  // namespace pf
