@@ -116,6 +116,7 @@ typedef struct {
   long long solves;             /* linear solves (substeps + coarse steps)      */
   double last_fine_ms;          /* device time of the last fine-sweep launch    */
   double last_coarse_ms;        /* device time of the last coarse-kernel launch */
+  long long helper_launches;    /* fine sweeps that ran with far-history helper CTAs */
 } pf_stats;
 
 /* ---- lifecycle ---------------------------------------------------------- */

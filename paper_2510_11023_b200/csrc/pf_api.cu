@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -79,6 +80,11 @@ struct pf_ctx {
   double guard = 0;
   bool parareal_ready = false;
   int pending_lo = -1, pending_bs = 0;  // last async fine launch, decoded by pf_dev_check
+  int* d_sync = nullptr;                 // sweep progress / ready / abort flags
+  int sync_cap = 0;
+  int num_sms = 0;
+  int allow_helpers = 1;  // PF_NO_HELPERS=1 forces the inline far history
+  int last_helpers = 0;
 };
 
 namespace {
@@ -187,16 +193,39 @@ int ensure_status(pf_ctx* c, int n) {
 }
 
 // Launch the fine sweep for slices [n_lo, n_lo+bs) reading device states d_u.
+// When 2*bs CTAs fit on the device at once, launch cooperatively with one
+// helper CTA per slice (far history on otherwise idle SMs); else inline.
 int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, Status* d_st) {
   if (c->paths.ensure((size_t)bs * (c->grid.m + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "paths");
-  if (c->scratch.ensure((size_t)bs * 2 * pf::HB * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
+  if (c->scratch.ensure((size_t)bs * 4 * pf::HB * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
+  if (c->sync_cap < bs) {
+    if (c->d_sync) cudaFree(c->d_sync);
+    c->d_sync = nullptr;
+    c->sync_cap = 0;
+    PF_CUDA(c, cudaMalloc(&c->d_sync, sizeof(int) * 3 * bs));
+    c->sync_cap = bs;
+  }
+  pf::SweepSync sync{c->d_sync, c->d_sync + bs, c->d_sync + 2 * bs};
+  PF_CUDA(c, cudaMemsetAsync(c->d_sync, 0, sizeof(int) * 3 * bs, c->stream));
   pf::Common cm = make_common(c);
   double* dp = c->paths.p;
   PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
   PF_DISPATCH(c, {
     auto kern = pf::k_fine_sweep<SP, SPP, NT, EPT>;
     PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
-    kern<<<bs, NT, c->smem, c->stream>>>(cm, spp, d_u, n_lo, dp, d_out, d_st);
+    int per_sm = 0;
+    PF_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, c->smem));
+    int helpers = (c->allow_helpers && 2 * bs <= per_sm * c->num_sms) ? 1 : 0;
+    int nsl = bs;
+    if (helpers) {
+      void* args[] = {(void*)&cm, (void*)&spp, (void*)&d_u, (void*)&n_lo, (void*)&nsl, (void*)&helpers,
+                      (void*)&sync, (void*)&dp, (void*)&d_out, (void*)&d_st};
+      PF_CUDA(c, cudaLaunchCooperativeKernel((void*)kern, dim3(2 * bs), dim3(NT), args, c->smem, c->stream));
+    } else {
+      kern<<<bs, NT, c->smem, c->stream>>>(cm, spp, d_u, n_lo, nsl, 0, sync, dp, d_out, d_st);
+    }
+    c->last_helpers = helpers;
+    c->stats.helper_launches += helpers;
   });
   PF_CUDA(c, cudaGetLastError());
   PF_CUDA(c, cudaEventRecord(c->ev1, c->stream));
@@ -340,7 +369,7 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
     c->size = M;
     static const Variant by_lg[12] = {V_NONE, V_NONE, V_S2, V_S3, V_S4, V_S5, V_S6, V_S7, V_S8, V_S9, V_S10, V_S11};
     c->variant = by_lg[c->lgQ];
-    c->smem = sizeof(cd) * (pf::tw_table_size(c->lgQ) + 3 * c->Q) + sizeof(double) * (c->Q + 128);
+    c->smem = sizeof(cd) * (pf::tw_table_size(c->lgQ) + 3 * c->Q) + sizeof(double) * (3 * c->Q + 128);
   } else if (space->kind == PF_SPACE_CHEB1D) {
     const int deg = space->modes;
     if (deg < 2) return set_error(c, PF_ERR_ARGUMENT, "degree must be at least 2 so interior nodes exist");
@@ -392,6 +421,11 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
   c->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaSetDevice");
+  PF_CUDA(c, cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  {
+    const char* env = std::getenv("PF_NO_HELPERS");
+    c->allow_helpers = (env && env[0] == '1') ? 0 : 1;
+  }
   PF_CUDA(c, cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
   c->stream = c->own_stream;
   PF_CUDA(c, cudaEventCreate(&c->ev0));
@@ -449,7 +483,7 @@ void pf_destroy(pf_ctx* c) {
   if (c->device >= 0) cudaSetDevice(c->device);
   for (DevBuf* b : {&c->U, &c->Unext, &c->paths, &c->fold, &c->gold, &c->gnew, &c->io, &c->scalar, &c->scratch}) b->release();
   for (void* p : {(void*)c->d_bfine, (void*)c->d_afine, (void*)c->d_bfrac, (void*)c->d_nodes, (void*)c->d_d1, (void*)c->d_qw,
-                  (void*)c->d_tw, (void*)c->d_ph, (void*)c->d_status})
+                  (void*)c->d_tw, (void*)c->d_ph, (void*)c->d_status, (void*)c->d_sync})
     if (p) cudaFree(p);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);

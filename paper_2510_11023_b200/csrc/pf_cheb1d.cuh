@@ -79,8 +79,8 @@ struct Cheb1D {
     return s;
   }
 
-  __device__ int step(const Fn& fn, const double* xprev, double t, double gam, const double* hist,
-                      const double* contrib, double* xout, Status& st) {
+  __device__ int step(const Fn& fn, const double* xprev, const double* /*xguess: direct solve*/, double t,
+                      double gam, const double* hist, const double* contrib, double* xout, Status& st) {
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int e = threadIdx.x + i * NT;
@@ -109,11 +109,12 @@ struct Cheb1D {
       aug[i * LD + j] = val;
       smax = fmax(smax, fabs(val));
     }
+    const double emt = exp(-t);
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int e = threadIdx.x + i * NT;
       if (e < ni) {
-        const double f = fn_f(fn, nodes[e + 1], 0.0, t, xprev[i]);
+        const double f = fn_f(fn, fn_xtab(nodes[e + 1]), emt, xprev[i]);
         aug[e * LD + ni] = __dadd_rn(__dadd_rn(hist[i], __dmul_rn(gam, f)), contrib[i]);
         perm[e] = e;
       }

@@ -61,14 +61,18 @@ __device__ __forceinline__ double fn_D(const Fn& f, double x, double x2, double 
   }
 }
 
-__device__ __forceinline__ double fn_f(const Fn& f, double x, double x2, double t, double u) {
+// x-only factors are tabulated once per kernel (sx = {sin(pi x), sin(2 pi x)})
+// and exp(-t) once per substep (emt), so the per-point cost is the u-dependent part.
+__device__ __forceinline__ double2 fn_xtab(double x) { return make_double2(sin(CUDART_PI * x), sin(2.0 * CUDART_PI * x)); }
+
+__device__ __forceinline__ double fn_f(const Fn& f, double2 sx, double emt, double u) {
   switch (f.id) {
     case 1:
-      return __dadd_rn(__dmul_rn(f.p[2], u), __dmul_rn(f.p[3], __dmul_rn(sin(CUDART_PI * x), exp(-t))));
+      return __dadd_rn(__dmul_rn(f.p[2], u), __dmul_rn(f.p[3], __dmul_rn(sx.x, emt)));
     case 2:
-      return sin(CUDART_PI * x) * cos(u);
+      return sx.x * cos(u);
     case 3:
-      return -u + 0.1 * sin(2.0 * CUDART_PI * x);
+      return -u + 0.1 * sx.y;
     case 4: {
       const double u2 = u * u;
       return u * (1.0 - u2) / (1.0 + u2);

@@ -30,17 +30,20 @@ struct Common {
 constexpr int HB = 16;
 
 // Far history for the HB target rows r = R0+1 .. R0+HB of one slice
-// (the einsum of stepping.py:234 restricted to j <= R0):
-//   out[rr] = b_{R0+rr} path[0] + sum_{j=1}^{R0} a_{R0+1+rr-j} path[j]
+// (the einsum of stepping.py:234 restricted to j <= Jmax):
+//   out[rr] = b_{R0+rr} path[0] + sum_{j=1}^{Jmax} a_{R0+1+rr-j} path[j]
 // Weights are Toeplitz in (r, j): a J-row chunk needs HB+J-1 of them.
+// Path rows are read through L2 (ld.global.cg): a helper CTA reads rows
+// another CTA wrote during this launch.
 template <int NT, int EPT, int J>
-__device__ __forceinline__ void far_history_block(const Common& c, const double* path, int R0, double* out) {
+__device__ __forceinline__ void far_history_block(const Common& c, const double* path, int R0, int Jmax,
+                                                  double* out) {
   double acc[HB][EPT];
   double c0[EPT];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int e = threadIdx.x + i * NT;
-    c0[i] = (e < c.size) ? path[e] : 0.0;
+    c0[i] = (e < c.size) ? __ldcg(path + e) : 0.0;
   }
 #pragma unroll
   for (int rr = 0; rr < HB; ++rr) {
@@ -48,7 +51,7 @@ __device__ __forceinline__ void far_history_block(const Common& c, const double*
 #pragma unroll
     for (int i = 0; i < EPT; ++i) acc[rr][i] = w * c0[i];
   }
-  for (int j0 = 1; j0 <= R0; j0 += J) {
+  for (int j0 = 1; j0 <= Jmax; j0 += J) {
     double cv[J][EPT];
 #pragma unroll
     for (int t = 0; t < J; ++t) {
@@ -56,7 +59,7 @@ __device__ __forceinline__ void far_history_block(const Common& c, const double*
 #pragma unroll
       for (int i = 0; i < EPT; ++i) {
         const int e = threadIdx.x + i * NT;
-        cv[t][i] = (e < c.size && j0 + t <= R0) ? row[e] : 0.0;
+        cv[t][i] = (e < c.size && j0 + t <= Jmax) ? __ldcg(row + e) : 0.0;
       }
     }
     // wv[u] = a_{R0+1-j0-(J-1)+u}, u = rr - t + J - 1
@@ -179,33 +182,114 @@ __device__ __forceinline__ void coarse_bracket(const Common& c, const double* __
   }
 }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// thread 0 waits until *flag >= v, then the whole CTA proceeds
+__device__ __forceinline__ void cta_wait_geq(const int* flag, int v) {
+  if (threadIdx.x == 0) {
+    int ns = 64;
+    while (ld_acquire(flag) < v) {
+      __nanosleep(ns);
+      ns = ns < 2048 ? 2 * ns : ns;
+    }
+  }
+  __syncthreads();
+}
+// the whole CTA's prior global writes become visible, then thread 0 publishes v
+__device__ __forceinline__ void cta_publish(int* flag, int v) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(flag, v);
+  }
+}
+
+// History rows of block beta (target rows R0+1..R0+HB, R0 = beta*HB) folded
+// into the far part: j <= J(beta) = max(beta-1, 0)*HB.  The lag of one block
+// lets a helper CTA compute block beta+1 while the slice CTA marches block beta.
+__device__ __forceinline__ int far_extent(int beta) { return (beta > 0 ? beta - 1 : 0) * HB; }
+
+struct SweepSync {
+  int* progress;  // [slice] last substep whose state row is in the path
+  int* ready;     // [slice] number of far-history blocks published
+  int* abort;     // [slice] set by a failing slice CTA
+};
+
+// Fine sweep.  Grid = nslices slice CTAs (+ nslices helper CTAs when
+// `helpers`, launched cooperatively so all are co-resident).  A helper owns
+// the far L1 history and the coarse-history bracket of its slice: it runs the
+// register-tiled Toeplitz GEMM for block beta+1 on an otherwise idle SM while
+// the slice CTA marches block beta, and publishes it with release/acquire
+// flags.  Without helpers the slice CTA computes the same blocks inline (same
+// code, same summation order: results are bitwise identical either way).
 template <class SP, class SPP, int NT, int EPT>
 __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const double* __restrict__ U, int n_lo,
-                                                   double* paths, double* __restrict__ out,
-                                                   Status* __restrict__ status) {
+                                                   int nslices, int helpers, SweepSync sync, double* paths,
+                                                   double* __restrict__ out, Status* __restrict__ status) {
   extern __shared__ __align__(16) char smem[];
-  SP sp;
-  sp.init(smem, spp);
-  const int b = blockIdx.x;
+  constexpr int JT = (EPT > 2 ? 4 : 8);
+  const bool helper = (int)blockIdx.x >= nslices;
+  const int b = helper ? (int)blockIdx.x - nslices : (int)blockIdx.x;
   const int n = n_lo + b;
   double* path = paths + (size_t)b * (c.m + 1) * c.size;
+  double* scr = c.scratch + (size_t)b * 4 * HB * c.size;  // [parity][hist|bracket][HB][size]
+  const int nblocks = (c.m + HB - 1) / HB;
+  if (helper) {
+    // path row 0 is the slice's start state, readable from U directly
+    for (int beta = 0; beta < nblocks; ++beta) {
+      const int J = far_extent(beta);
+      if (J > 0) {
+        if (threadIdx.x == 0) {
+          int ns = 64;
+          while (ld_acquire(sync.progress + b) < J && ld_acquire(sync.abort + b) == 0) {
+            __nanosleep(ns);
+            ns = ns < 2048 ? 2 * ns : ns;
+          }
+        }
+        __syncthreads();
+        if (ld_acquire(sync.abort + b) != 0) return;
+      }
+      double* hs = scr + (size_t)(beta & 1) * 2 * HB * c.size;
+      far_history_block<NT, EPT, JT>(c, J > 0 ? path : U + (size_t)n * c.size, beta * HB, J, hs);
+      bracket_block<NT, EPT>(c, U, n, beta * HB + 1, hs + (size_t)HB * c.size);
+      cta_publish(sync.ready + b, beta + 1);
+    }
+    return;
+  }
+  SP sp;
+  sp.init(smem, spp);
   Status st = {ST_OK, n, 0, -1, 0, 0, {0, 0}};
-  double x[EPT];
+  double x[EPT], xpp[EPT];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int e = threadIdx.x + i * NT;
     x[i] = (e < c.size) ? U[(size_t)n * c.size + e] : 0.0;
+    xpp[i] = x[i];
     if (e < c.size) path[e] = x[i];
   }
-  double* hscr = c.scratch + (size_t)b * 2 * HB * c.size;
-  double* cscr = hscr + (size_t)HB * c.size;
+  const double* hs = nullptr;
+  int J = 0;
   for (int r = 1; r <= c.m; ++r) {
     const double t = (double)n * c.dT + (double)(r - 1) * c.dt;
     const int rr = (r - 1) % HB;
-    const int R0 = r - 1 - rr;
+    const int beta = (r - 1) / HB;
     if (rr == 0) {
-      far_history_block<NT, EPT, (EPT > 2 ? 4 : 8)>(c, path, R0, hscr);
-      bracket_block<NT, EPT>(c, U, n, r, cscr);
+      J = far_extent(beta);
+      double* slot = scr + (size_t)(beta & 1) * 2 * HB * c.size;
+      if (helpers) {
+        cta_publish(sync.progress + b, r - 1);  // rows 0..r-1 are in the path
+        cta_wait_geq(sync.ready + b, beta + 1);
+      } else {
+        far_history_block<NT, EPT, JT>(c, path, beta * HB, J, slot);
+        bracket_block<NT, EPT>(c, U, n, r, slot + (size_t)HB * c.size);
+      }
+      hs = slot;
     }
     double h[EPT], ct[EPT], xn[EPT];
 #pragma unroll
@@ -213,14 +297,17 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       const int e = threadIdx.x + i * NT;
       double acc = 0.0, cb = 0.0;
       if (e < c.size) {
-        acc = hscr[(size_t)rr * c.size + e];
-        for (int j = R0 + 1; j < r; ++j) acc = fma(c.afine[r - j], path[(size_t)j * c.size + e], acc);
-        cb = cscr[(size_t)rr * c.size + e];
+        acc = __ldcg(hs + (size_t)rr * c.size + e);
+        for (int j = J + 1; j < r; ++j) acc = fma(c.afine[r - j], path[(size_t)j * c.size + e], acc);
+        cb = __ldcg(hs + (size_t)(HB + rr) * c.size + e);
       }
       h[i] = acc;
       ct[i] = cb;
     }
-    const int code = sp.step(c.fn, x, t, c.gam_f, h, ct, xn, st);
+    double xg[EPT];  // linear extrapolation of the path: PCG initial guess
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) xg[i] = (r > 1) ? fma(2.0, x[i], -xpp[i]) : x[i];
+    const int code = sp.step(c.fn, x, xg, t, c.gam_f, h, ct, xn, st);
     if (code != ST_OK) {
       st.code = code;
       st.r = r;
@@ -229,6 +316,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int e = threadIdx.x + i * NT;
+      xpp[i] = x[i];
       x[i] = xn[i];
       if (e < c.size) path[(size_t)r * c.size + e] = x[i];
     }
@@ -239,6 +327,8 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       const int e = threadIdx.x + i * NT;
       if (e < c.size) out[(size_t)b * c.size + e] = x[i];
     }
+  } else if (helpers && threadIdx.x == 0) {
+    st_release(sync.abort + b, 1);
   }
   if (threadIdx.x == 0) status[b] = st;
 }
@@ -262,7 +352,7 @@ __device__ __forceinline__ int coarse_apply(SP& sp, const Common& c, const doubl
       xp[i] = H[(size_t)n * c.size + e];
     }
   }
-  return sp.step(c.fn, xp, (double)n * c.dT, c.gam_c, h, z, xout, st);
+  return sp.step(c.fn, xp, xp, (double)n * c.dT, c.gam_c, h, z, xout, st);
 }
 
 enum CoarseMode : int { CM_RUN = 0, CM_CORRECT = 1, CM_SINGLE = 2 };
@@ -388,11 +478,12 @@ __global__ void __launch_bounds__(NT) k_sequential(Common c, SPP spp, double* hi
   SP sp;
   sp.init(smem, spp);
   Status st = {ST_OK, 0, -1, -1, 0, 0, {0, 0}};
-  double x[EPT];
+  double x[EPT], xpp[EPT];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int e = threadIdx.x + i * NT;
     x[i] = (e < c.size) ? hist[e] : 0.0;
+    xpp[i] = x[i];
   }
   for (int jj = 1; jj <= total; ++jj) {
     double h[EPT], z[EPT], xn[EPT];
@@ -400,7 +491,10 @@ __global__ void __launch_bounds__(NT) k_sequential(Common c, SPP spp, double* hi
 #pragma unroll
     for (int i = 0; i < EPT; ++i) z[i] = 0.0;
     st.n = jj - 1;
-    const int code = sp.step(c.fn, x, (double)(jj - 1) * c.dt, c.gam_f, h, z, xn, st);
+    double xg[EPT];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) xg[i] = (jj > 1) ? fma(2.0, x[i], -xpp[i]) : x[i];
+    const int code = sp.step(c.fn, x, xg, (double)(jj - 1) * c.dt, c.gam_f, h, z, xn, st);
     if (code != ST_OK) {
       st.code = code;
       break;
@@ -408,6 +502,7 @@ __global__ void __launch_bounds__(NT) k_sequential(Common c, SPP spp, double* hi
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int e = threadIdx.x + i * NT;
+      xpp[i] = x[i];
       x[i] = xn[i];
       if (e < c.size) hist[(size_t)jj * c.size + e] = x[i];
     }

@@ -132,11 +132,12 @@ struct Sine1D {
   const cd* ph;
   cd *A, *B;
   double* dq;
+  double2* xtab;  // {sin(pi x_q), sin(2 pi x_q)}
   Reducer<NT> red;
   double tol2;
   int maxit;
 
-  static size_t smem_bytes() { return sizeof(cd) * (TW + 3 * Q) + sizeof(double) * (Q + 128); }
+  static size_t smem_bytes() { return sizeof(cd) * (TW + 3 * Q) + sizeof(double) * (3 * Q + 128); }
 
   __device__ void init(char* smem, const Sine1DParams& p) {
     cd* s = reinterpret_cast<cd*>(smem);
@@ -145,9 +146,13 @@ struct Sine1D {
     A = phs + Q;
     B = A + Q;
     dq = reinterpret_cast<double*>(B + Q);
-    red.init(dq + Q);
+    xtab = reinterpret_cast<double2*>(dq + Q);
+    red.init(reinterpret_cast<double*>(xtab + Q));
     for (int j = threadIdx.x; j < TW; j += NT) tws[j] = p.twp[j];
-    for (int j = threadIdx.x; j < Q; j += NT) phs[j] = p.ph[j];
+    for (int j = threadIdx.x; j < Q; j += NT) {
+      phs[j] = p.ph[j];
+      xtab[j] = fn_xtab(((double)j + 0.5) / (double)Q);
+    }
     twp = tws;
     ph = phs;
     tol2 = p.pcg_tol * p.pcg_tol;
@@ -230,15 +235,17 @@ struct Sine1D {
   }
 
   // One semi-implicit substep.  xprev: owned coefficients of c_prev.
-  __device__ int step(const Fn& fn, const double* xprev, double t, double gam, const double* hist,
-                      const double* contrib, double* xout, Status& st) {
-    // --- synthesis pair: u = S c, v0 = S' c -----------------------------
+  // xguess: PCG initial guess (the caller extrapolates from the path; it
+  // only changes the iteration count, not the solution beyond pcg_tol).
+  __device__ int step(const Fn& fn, const double* xprev, const double* xguess, double t, double gam,
+                      const double* hist, const double* contrib, double* xout, Status& st) {
+    // --- synthesis pair: u = S c_prev, v0 = S' x0 ------------------------
     {
       double av[EPT], bv[EPT];
 #pragma unroll
       for (int i = 0; i < EPT; ++i) {
         av[i] = SQ2 * xprev[i];
-        bv[i] = SQ2 * CUDART_PI * (double)mode(i) * xprev[i];
+        bv[i] = SQ2 * CUDART_PI * (double)mode(i) * xguess[i];
       }
       synth_input(av, bv);
     }
@@ -247,6 +254,7 @@ struct Sine1D {
     cd* O = (R == A) ? B : A;
     // --- pointwise coefficients (fused epilogue) ------------------------
     const double wq = 1.0 / (double)Q;
+    const double emt = exp(-t);
     double dsum = 0.0, nbad = 0.0;
     int bad = 0x7fffffff;
 #pragma unroll
@@ -264,7 +272,7 @@ struct Sine1D {
           nbad += 1.0;
         }
         const double d = wq * Dv;
-        const double g = wq * fn_f(fn, xq, 0.0, t, u);
+        const double g = wq * fn_f(fn, xtab[q], emt, u);
         dq[q] = d;
         dsum += d;
         R[s] = {(q & 1) ? -g : g, d * s2};
@@ -276,7 +284,7 @@ struct Sine1D {
       return ST_COEFF;
     }
     const double dbar = s01.x;
-    // --- analysis pair: F = S^T g, K c_prev = S'^T (d v0) ----------------
+    // --- analysis pair: F = S^T g, K x0 = S'^T (d v0) --------------------
     cd* Z = fft_stockham<LG, NT, false>(R, O, twp);
     double x[EPT], r[EPT], p[EPT], z[EPT], pinv[EPT];
     double bb = 0.0, rr = 0.0;
@@ -292,7 +300,7 @@ struct Sine1D {
         const double F = SQ2 * X1;
         const double kx = SQ2 * CUDART_PI * (double)k * X2;
         const double rhs = __dadd_rn(__dadd_rn(hist[i], __dmul_rn(gam, F)), contrib[i]);
-        x[i] = xprev[i];
+        x[i] = xguess[i];
         r[i] = rhs - (x[i] + gam * kx);
         const double kk = (double)k;
         pinv[i] = 1.0 / (1.0 + gam * dbar * (CUDART_PI * CUDART_PI) * (kk * kk));
