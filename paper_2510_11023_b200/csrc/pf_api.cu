@@ -215,14 +215,25 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
     PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
     int per_sm = 0;
     PF_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, c->smem));
+    // shared-memory ring of the last NR states behind the space's own smem
+    const size_t ring_bytes = sizeof(double) * pf::NR * c->size;
+    const size_t base = (c->smem + 15) & ~size_t(15);
+    int ring_off = -1;
+    size_t smem = c->smem;
+    if (base + ring_bytes <= 227 * 1024) {
+      ring_off = (int)base;
+      smem = base + ring_bytes;
+    }
+    PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PF_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     int helpers = (c->allow_helpers && 2 * bs <= per_sm * c->num_sms) ? 1 : 0;
     int nsl = bs;
     if (helpers) {
       void* args[] = {(void*)&cm, (void*)&spp, (void*)&d_u, (void*)&n_lo, (void*)&nsl, (void*)&helpers,
-                      (void*)&sync, (void*)&dp, (void*)&d_out, (void*)&d_st};
-      PF_CUDA(c, cudaLaunchCooperativeKernel((void*)kern, dim3(2 * bs), dim3(NT), args, c->smem, c->stream));
+                      (void*)&ring_off, (void*)&sync, (void*)&dp, (void*)&d_out, (void*)&d_st};
+      PF_CUDA(c, cudaLaunchCooperativeKernel((void*)kern, dim3(2 * bs), dim3(NT), args, smem, c->stream));
     } else {
-      kern<<<bs, NT, c->smem, c->stream>>>(cm, spp, d_u, n_lo, nsl, 0, sync, dp, d_out, d_st);
+      kern<<<bs, NT, smem, c->stream>>>(cm, spp, d_u, n_lo, nsl, 0, ring_off, sync, dp, d_out, d_st);
     }
     c->last_helpers = helpers;
     c->stats.helper_launches += helpers;

@@ -27,7 +27,13 @@ struct Common {
 
 // Block length of the blocked L1 history: each history row is read once per
 // HB substeps and reused for HB target rows (register-tiled Toeplitz GEMM).
-constexpr int HB = 16;
+constexpr int HB = 8;
+// The last NR states of a slice live in a shared-memory ring (when it fits):
+// the near history (< 2*HB rows) and the PCG initial guess read it there.
+constexpr int NR = 2 * HB;
+// PCG initial guess: order-EXO polynomial extrapolation of the path,
+// x0 = sum_j (-1)^j C(p+1, j+1) c_{r-1-j}, p = min(EXO, r-1).
+constexpr int EXO = 5;
 
 // Far history for the HB target rows r = R0+1 .. R0+HB of one slice
 // (the einsum of stepping.py:234 restricted to j <= Jmax):
@@ -230,7 +236,8 @@ struct SweepSync {
 // code, same summation order: results are bitwise identical either way).
 template <class SP, class SPP, int NT, int EPT>
 __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const double* __restrict__ U, int n_lo,
-                                                   int nslices, int helpers, SweepSync sync, double* paths,
+                                                   int nslices, int helpers, int ring_off, SweepSync sync,
+                                                   double* paths,
                                                    double* __restrict__ out, Status* __restrict__ status) {
   extern __shared__ __align__(16) char smem[];
   constexpr int JT = (EPT > 2 ? 4 : 8);
@@ -264,14 +271,17 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   }
   SP sp;
   sp.init(smem, spp);
+  double* ring = ring_off >= 0 ? reinterpret_cast<double*>(smem + ring_off) : nullptr;
   Status st = {ST_OK, n, 0, -1, 0, 0, {0, 0}};
-  double x[EPT], xpp[EPT];
+  double x[EPT];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int e = threadIdx.x + i * NT;
     x[i] = (e < c.size) ? U[(size_t)n * c.size + e] : 0.0;
-    xpp[i] = x[i];
-    if (e < c.size) path[e] = x[i];
+    if (e < c.size) {
+      path[e] = x[i];
+      if (ring) ring[e] = x[i];
+    }
   }
   const double* hs = nullptr;
   int J = 0;
@@ -291,22 +301,33 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       }
       hs = slot;
     }
-    double h[EPT], ct[EPT], xn[EPT];
+    const int p = r - 1 < EXO ? r - 1 : EXO;
+    double h[EPT], ct[EPT], xg[EPT], xn[EPT];
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int e = threadIdx.x + i * NT;
-      double acc = 0.0, cb = 0.0;
+      double acc = 0.0, cb = 0.0, g = x[i];
       if (e < c.size) {
         acc = __ldcg(hs + (size_t)rr * c.size + e);
-        for (int j = J + 1; j < r; ++j) acc = fma(c.afine[r - j], path[(size_t)j * c.size + e], acc);
+        for (int j = J + 1; j < r; ++j) {
+          const double v = ring ? ring[(size_t)(j & (NR - 1)) * c.size + e] : path[(size_t)j * c.size + e];
+          acc = fma(c.afine[r - j], v, acc);
+        }
         cb = __ldcg(hs + (size_t)(HB + rr) * c.size + e);
+        // extrapolated guess; row r-1 is x itself
+        double bin = (double)(p + 1);  // C(p+1, 1)
+        g = bin * x[i];
+        for (int j = 1; j <= p; ++j) {
+          bin = bin * (double)(p + 1 - j) / (double)(j + 1);  // C(p+1, j+1)
+          const int row = r - 1 - j;
+          const double v = ring ? ring[(size_t)(row & (NR - 1)) * c.size + e] : path[(size_t)row * c.size + e];
+          g = (j & 1) ? fma(-bin, v, g) : fma(bin, v, g);
+        }
       }
       h[i] = acc;
       ct[i] = cb;
+      xg[i] = g;
     }
-    double xg[EPT];  // linear extrapolation of the path: PCG initial guess
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) xg[i] = (r > 1) ? fma(2.0, x[i], -xpp[i]) : x[i];
     const int code = sp.step(c.fn, x, xg, t, c.gam_f, h, ct, xn, st);
     if (code != ST_OK) {
       st.code = code;
@@ -316,9 +337,11 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int e = threadIdx.x + i * NT;
-      xpp[i] = x[i];
       x[i] = xn[i];
-      if (e < c.size) path[(size_t)r * c.size + e] = x[i];
+      if (e < c.size) {
+        path[(size_t)r * c.size + e] = x[i];
+        if (ring) ring[(size_t)(r & (NR - 1)) * c.size + e] = x[i];
+      }
     }
   }
   if (st.code == ST_OK) {
