@@ -127,6 +127,7 @@ pf::Common make_common(const pf_ctx* c) {
   cm.afine = c->d_afine;
   cm.bfrac = c->d_bfrac;
   cm.scratch = c->scratch.p;
+  for (int s = 0; s < 16; ++s) cm.anear[s] = (s >= 1 && s < (long)c->h_bfine.size()) ? c->h_bfine[s - 1] - c->h_bfine[s] : 0.0;
   return cm;
 }
 
@@ -229,11 +230,12 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
     int helpers = (c->allow_helpers && 2 * bs <= per_sm * c->num_sms) ? 1 : 0;
     int nsl = bs;
     if (helpers) {
+      int smem_total = (int)smem;
       void* args[] = {(void*)&cm, (void*)&spp, (void*)&d_u, (void*)&n_lo, (void*)&nsl, (void*)&helpers,
-                      (void*)&ring_off, (void*)&sync, (void*)&dp, (void*)&d_out, (void*)&d_st};
+                      (void*)&ring_off, (void*)&smem_total, (void*)&sync, (void*)&dp, (void*)&d_out, (void*)&d_st};
       PF_CUDA(c, cudaLaunchCooperativeKernel((void*)kern, dim3(2 * bs), dim3(NT), args, smem, c->stream));
     } else {
-      kern<<<bs, NT, smem, c->stream>>>(cm, spp, d_u, n_lo, nsl, 0, ring_off, sync, dp, d_out, d_st);
+      kern<<<bs, NT, smem, c->stream>>>(cm, spp, d_u, n_lo, nsl, 0, ring_off, (int)smem, sync, dp, d_out, d_st);
     }
     c->last_helpers = helpers;
     c->stats.helper_launches += helpers;

@@ -23,6 +23,7 @@ struct Common {
   const double* afine;                // a_s = b_{s-1} - b_s (s >= 1; a_0 unused)
   const double* bfrac;                // b_{q/m}
   double* scratch;                    // per-slice block history / bracket rows
+  double anear[16];                   // a_s for s < 16 (near-history weights, uniform loads)
 };
 
 // Block length of the blocked L1 history: each history row is read once per
@@ -34,16 +35,55 @@ constexpr int NR = 2 * HB;
 // PCG initial guess: order-EXO polynomial extrapolation of the path,
 // x0 = sum_j (-1)^j C(p+1, j+1) c_{r-1-j}, p = min(EXO, r-1).
 constexpr int EXO = 5;
+// kExtrap[p][j] = (-1)^j C(p+1, j+1)
+__constant__ double kExtrap[EXO + 1][EXO + 1] = {
+    {1, 0, 0, 0, 0, 0},        {2, -1, 0, 0, 0, 0},        {3, -3, 1, 0, 0, 0},
+    {4, -6, 4, -1, 0, 0},      {5, -10, 10, -5, 1, 0},     {6, -15, 20, -15, 6, -1}};
 
 // Far history for the HB target rows r = R0+1 .. R0+HB of one slice
 // (the einsum of stepping.py:234 restricted to j <= Jmax):
 //   out[rr] = b_{R0+rr} path[0] + sum_{j=1}^{Jmax} a_{R0+1+rr-j} path[j]
-// Weights are Toeplitz in (r, j): a J-row chunk needs HB+J-1 of them.
-// Path rows are read through L2 (ld.global.cg): a helper CTA reads rows
-// another CTA wrote during this launch.
+// Weights are Toeplitz in (r, j): a J-row chunk needs HB+J-1 of them, read
+// from `aw` (shared memory in helper CTAs).  Chunks are double-buffered in
+// registers so the next chunk's loads overlap this chunk's FMAs.  Path rows
+// are read through L2 (ld.global.cg): a helper CTA reads rows another CTA
+// wrote during this launch.
 template <int NT, int EPT, int J>
-__device__ __forceinline__ void far_history_block(const Common& c, const double* path, int R0, int Jmax,
-                                                  double* out) {
+__device__ __forceinline__ void load_rows(const Common& c, const double* path, int j0, int Jmax,
+                                          double (&cv)[J][EPT]) {
+#pragma unroll
+  for (int t = 0; t < J; ++t) {
+    const double* row = path + (size_t)(j0 + t) * c.size;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = threadIdx.x + i * NT;
+      cv[t][i] = (e < c.size && j0 + t <= Jmax) ? __ldcg(row + e) : 0.0;
+    }
+  }
+}
+
+template <int EPT, int J>
+__device__ __forceinline__ void fma_rows(const double* aw, int R0, int j0, const double (&cv)[J][EPT],
+                                         double (&acc)[HB][EPT]) {
+  // wv[u] = a_{R0+1-j0-(J-1)+u}, u = rr - t + J - 1 (index clamped for rows past Jmax, whose data is 0)
+  double wv[HB + J - 1];
+  const int s0 = R0 + 1 - j0 - (J - 1);
+#pragma unroll
+  for (int u = 0; u < HB + J - 1; ++u) {
+    const int s = s0 + u;
+    wv[u] = aw[s < 1 ? 1 : s];
+  }
+#pragma unroll
+  for (int t = 0; t < J; ++t)
+#pragma unroll
+    for (int rr = 0; rr < HB; ++rr)
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) acc[rr][i] = fma(wv[rr - t + J - 1], cv[t][i], acc[rr][i]);
+}
+
+template <int NT, int EPT, int J>
+__device__ __forceinline__ void far_history_block(const Common& c, const double* path, const double* aw, int R0,
+                                                  int Jmax, double* out) {
   double acc[HB][EPT];
   double c0[EPT];
 #pragma unroll
@@ -57,31 +97,16 @@ __device__ __forceinline__ void far_history_block(const Common& c, const double*
 #pragma unroll
     for (int i = 0; i < EPT; ++i) acc[rr][i] = w * c0[i];
   }
-  for (int j0 = 1; j0 <= Jmax; j0 += J) {
-    double cv[J][EPT];
-#pragma unroll
-    for (int t = 0; t < J; ++t) {
-      const double* row = path + (size_t)(j0 + t) * c.size;
-#pragma unroll
-      for (int i = 0; i < EPT; ++i) {
-        const int e = threadIdx.x + i * NT;
-        cv[t][i] = (e < c.size && j0 + t <= Jmax) ? __ldcg(row + e) : 0.0;
-      }
+  if (Jmax >= 1) {
+    double ca[J][EPT], cb[J][EPT];
+    load_rows<NT, EPT, J>(c, path, 1, Jmax, ca);
+    for (int j0 = 1; j0 <= Jmax; j0 += 2 * J) {
+      load_rows<NT, EPT, J>(c, path, j0 + J, Jmax, cb);
+      fma_rows<EPT, J>(aw, R0, j0, ca, acc);
+      if (j0 + J > Jmax) break;
+      load_rows<NT, EPT, J>(c, path, j0 + 2 * J, Jmax, ca);
+      fma_rows<EPT, J>(aw, R0, j0 + J, cb, acc);
     }
-    // wv[u] = a_{R0+1-j0-(J-1)+u}, u = rr - t + J - 1
-    double wv[HB + J - 1];
-    const int s0 = R0 + 1 - j0 - (J - 1);
-#pragma unroll
-    for (int u = 0; u < HB + J - 1; ++u) {
-      const int s = s0 + u;
-      wv[u] = c.afine[s < 1 ? 1 : s];
-    }
-#pragma unroll
-    for (int t = 0; t < J; ++t)
-#pragma unroll
-      for (int rr = 0; rr < HB; ++rr)
-#pragma unroll
-        for (int i = 0; i < EPT; ++i) acc[rr][i] = fma(wv[rr - t + J - 1], cv[t][i], acc[rr][i]);
   }
 #pragma unroll
   for (int rr = 0; rr < HB; ++rr)
@@ -236,11 +261,12 @@ struct SweepSync {
 // code, same summation order: results are bitwise identical either way).
 template <class SP, class SPP, int NT, int EPT>
 __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const double* __restrict__ U, int n_lo,
-                                                   int nslices, int helpers, int ring_off, SweepSync sync,
+                                                   int nslices, int helpers, int ring_off, int smem_total,
+                                                   SweepSync sync,
                                                    double* paths,
                                                    double* __restrict__ out, Status* __restrict__ status) {
   extern __shared__ __align__(16) char smem[];
-  constexpr int JT = (EPT > 2 ? 4 : 8);
+  constexpr int JT = (EPT > 2 ? 4 : 8);  // rows per register chunk (x2 double-buffered)
   const bool helper = (int)blockIdx.x >= nslices;
   const int b = helper ? (int)blockIdx.x - nslices : (int)blockIdx.x;
   const int n = n_lo + b;
@@ -248,6 +274,14 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   double* scr = c.scratch + (size_t)b * 4 * HB * c.size;  // [parity][hist|bracket][HB][size]
   const int nblocks = (c.m + HB - 1) / HB;
   if (helper) {
+    // Toeplitz weights a_s into shared memory once (helpers own the SM's smem)
+    const double* aw = c.afine;
+    if ((size_t)(c.m + HB + 1) * sizeof(double) <= (size_t)smem_total) {
+      double* s_aw = reinterpret_cast<double*>(smem);
+      for (int q = threadIdx.x; q <= c.m + HB; q += NT) s_aw[q] = c.afine[q];
+      __syncthreads();
+      aw = s_aw;
+    }
     // path row 0 is the slice's start state, readable from U directly
     for (int beta = 0; beta < nblocks; ++beta) {
       const int J = far_extent(beta);
@@ -263,7 +297,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         if (ld_acquire(sync.abort + b) != 0) return;
       }
       double* hs = scr + (size_t)(beta & 1) * 2 * HB * c.size;
-      far_history_block<NT, EPT, JT>(c, J > 0 ? path : U + (size_t)n * c.size, beta * HB, J, hs);
+      far_history_block<NT, EPT, JT>(c, J > 0 ? path : U + (size_t)n * c.size, aw, beta * HB, J, hs);
       bracket_block<NT, EPT>(c, U, n, beta * HB + 1, hs + (size_t)HB * c.size);
       cta_publish(sync.ready + b, beta + 1);
     }
@@ -296,7 +330,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         cta_publish(sync.progress + b, r - 1);  // rows 0..r-1 are in the path
         cta_wait_geq(sync.ready + b, beta + 1);
       } else {
-        far_history_block<NT, EPT, JT>(c, path, beta * HB, J, slot);
+        far_history_block<NT, EPT, JT>(c, path, c.afine, beta * HB, J, slot);
         bracket_block<NT, EPT>(c, U, n, r, slot + (size_t)HB * c.size);
       }
       hs = slot;
@@ -311,17 +345,16 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         acc = __ldcg(hs + (size_t)rr * c.size + e);
         for (int j = J + 1; j < r; ++j) {
           const double v = ring ? ring[(size_t)(j & (NR - 1)) * c.size + e] : path[(size_t)j * c.size + e];
-          acc = fma(c.afine[r - j], v, acc);
+          acc = fma(c.anear[r - j], v, acc);
         }
         cb = __ldcg(hs + (size_t)(HB + rr) * c.size + e);
         // extrapolated guess; row r-1 is x itself
-        double bin = (double)(p + 1);  // C(p+1, 1)
-        g = bin * x[i];
+        const double* w = kExtrap[p];
+        g = w[0] * x[i];
         for (int j = 1; j <= p; ++j) {
-          bin = bin * (double)(p + 1 - j) / (double)(j + 1);  // C(p+1, j+1)
           const int row = r - 1 - j;
           const double v = ring ? ring[(size_t)(row & (NR - 1)) * c.size + e] : path[(size_t)row * c.size + e];
-          g = (j & 1) ? fma(-bin, v, g) : fma(bin, v, g);
+          g = fma(w[j], v, g);
         }
       }
       h[i] = acc;
