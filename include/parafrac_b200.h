@@ -130,6 +130,8 @@ int pf_reset_stats(pf_ctx* ctx);
 /* cudaStream_t used by every launch (NULL = the context's own stream). */
 int pf_set_stream(pf_ctx* ctx, void* stream);
 const char* pf_version(void);
+/* development aid: per-phase cycle counters of slice 0 (zeros unless built with -DPF_PHASE_TIMING) */
+int pf_debug_phases(long long* out16, int reset);
 
 /* ---- host-buffer entry points (reference-facing) ------------------------ */
 /* stepping.coarse_step: history = states at coarse nodes 0..n_states-1 */

@@ -354,6 +354,21 @@ extern "C" {
 
 const char* pf_version(void) { return "parafrac_b200 0.1.0 (sm_100a)"; }
 
+// Phase cycle counters of slice 0 (only in -DPF_PHASE_TIMING builds; else 16 zeros).
+int pf_debug_phases(long long* out16, int reset) {
+#ifdef PF_PHASE_TIMING
+  if (cudaMemcpyFromSymbol(out16, pf::g_phase, sizeof(long long) * 16) != cudaSuccess) return PF_ERR_CUDA;
+  if (reset) {
+    long long z[16] = {0};
+    cudaMemcpyToSymbol(pf::g_phase, z, sizeof(z));
+  }
+#else
+  for (int i = 0; i < 16; ++i) out16[i] = 0;
+  (void)reset;
+#endif
+  return PF_OK;
+}
+
 int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* space, const pf_weights* weights,
               int device, pf_ctx** out) {
   if (!out) return PF_ERR_ARGUMENT;
@@ -382,7 +397,7 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
     c->size = M;
     static const Variant by_lg[12] = {V_NONE, V_NONE, V_S2, V_S3, V_S4, V_S5, V_S6, V_S7, V_S8, V_S9, V_S10, V_S11};
     c->variant = by_lg[c->lgQ];
-    c->smem = sizeof(cd) * (pf::tw_table_size(c->lgQ) + 3 * c->Q) + sizeof(double) * (3 * c->Q + 128);
+    c->smem = sizeof(cd) * (pf::tw_table_size(c->lgQ) + 3 * c->Q) + sizeof(double) * (4 * c->Q + pf::RED_DOUBLES);
   } else if (space->kind == PF_SPACE_CHEB1D) {
     const int deg = space->modes;
     if (deg < 2) return set_error(c, PF_ERR_ARGUMENT, "degree must be at least 2 so interior nodes exist");

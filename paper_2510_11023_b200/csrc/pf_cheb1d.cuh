@@ -38,7 +38,7 @@ struct Cheb1D {
   }
   static size_t smem_bytes(int degree) {
     const size_t npts = degree + 1, ni = degree - 1, ld = ld_of((int)ni);
-    return sizeof(double) * (npts * npts + 2 * npts + ni * ld + 3 * npts + ni + 4 + 128) + sizeof(int) * (ni + 4);
+    return sizeof(double) * (npts * npts + 2 * npts + ni * ld + 3 * npts + ni + 4 + RED_DOUBLES) + sizeof(int) * (ni + 4);
   }
 
   __device__ void init(char* smem, const Cheb1DParams& p) {
@@ -56,7 +56,7 @@ struct Cheb1D {
     pivs = xs + npts;
     double* rs = pivs + 4;
     red.init(rs);
-    perm = reinterpret_cast<int*>(rs + 128);
+    perm = reinterpret_cast<int*>(rs + RED_DOUBLES);
     for (int i = threadIdx.x; i < npts * npts; i += NT) d1s[i] = p.d1[i];
     for (int i = threadIdx.x; i < npts; i += NT) {
       nds[i] = p.nodes[i];

@@ -7,6 +7,25 @@
 
 namespace pf {
 
+// Optional phase timing of slice 0 (build with -DPF_PHASE_TIMING; read with
+// pf_debug_phases).  Compiled out of the product library.
+#ifdef PF_PHASE_TIMING
+__device__ long long g_phase[16];
+__device__ long long g_phase_last;
+#define PF_T(k)                                        \
+  do {                                                 \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {         \
+      const long long _t = clock64();                  \
+      g_phase[(k)] += _t - g_phase_last;               \
+      g_phase_last = _t;                               \
+    }                                                  \
+  } while (0)
+#else
+#define PF_T(k) \
+  do {          \
+  } while (0)
+#endif
+
 struct cd {
   double x, y;
 };
@@ -84,8 +103,10 @@ __device__ __forceinline__ double fn_f(const Fn& f, double2 sx, double emt, doub
 
 // ---------------------------------------------------------------------------
 // deterministic block reductions (fixed order; every thread gets the total)
-// `red` holds 2 buffers x 32 warps x 2 values.  One __syncthreads each.
+// `red` holds 2 buffers x 32 warps x 4 values (RED_DOUBLES).  One __syncthreads each.
 // ---------------------------------------------------------------------------
+constexpr int RED_DOUBLES = 256;
+
 template <int NT>
 struct Reducer {
   double* red;
@@ -106,20 +127,49 @@ struct Reducer {
       return make_double2(a, b);
     }
     const int w = threadIdx.x >> 5;
-    double* slot = red + buf * 64;
+    double* slot = red + buf * 128;
     if ((threadIdx.x & 31) == 0) {
-      slot[2 * w] = a;
-      slot[2 * w + 1] = b;
+      slot[4 * w] = a;
+      slot[4 * w + 1] = b;
     }
     __syncthreads();
     double sa = 0.0, sb = 0.0;
 #pragma unroll
     for (int i = 0; i < NT / 32; ++i) {
-      sa += slot[2 * i];
-      sb += slot[2 * i + 1];
+      sa += slot[4 * i];
+      sb += slot[4 * i + 1];
     }
     buf ^= 1;
     return make_double2(sa, sb);
+  }
+  __device__ __forceinline__ double3 sum3(double a, double b, double c) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    if (NT == 32) {
+      __syncwarp();
+      return make_double3(a, b, c);
+    }
+    const int w = threadIdx.x >> 5;
+    double* slot = red + buf * 128;
+    if ((threadIdx.x & 31) == 0) {
+      slot[4 * w] = a;
+      slot[4 * w + 1] = b;
+      slot[4 * w + 2] = c;
+    }
+    __syncthreads();
+    double sa = 0.0, sb = 0.0, sc = 0.0;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) {
+      sa += slot[4 * i];
+      sb += slot[4 * i + 1];
+      sc += slot[4 * i + 2];
+    }
+    buf ^= 1;
+    return make_double3(sa, sb, sc);
   }
   __device__ __forceinline__ double sum(double a) { return sum2(a, 0.0).x; }
   __device__ __forceinline__ double max(double a) {
@@ -130,12 +180,12 @@ struct Reducer {
       return a;
     }
     const int w = threadIdx.x >> 5;
-    double* slot = red + buf * 64;
-    if ((threadIdx.x & 31) == 0) slot[2 * w] = a;
+    double* slot = red + buf * 128;
+    if ((threadIdx.x & 31) == 0) slot[4 * w] = a;
     __syncthreads();
     double s = slot[0];
 #pragma unroll
-    for (int i = 1; i < NT / 32; ++i) s = fmax(s, slot[2 * i]);
+    for (int i = 1; i < NT / 32; ++i) s = fmax(s, slot[4 * i]);
     buf ^= 1;
     return s;
   }
@@ -148,12 +198,12 @@ struct Reducer {
       return a;
     }
     const int w = threadIdx.x >> 5;
-    double* slot = red + buf * 64;
-    if ((threadIdx.x & 31) == 0) slot[2 * w] = (double)a;
+    double* slot = red + buf * 128;
+    if ((threadIdx.x & 31) == 0) slot[4 * w] = (double)a;
     __syncthreads();
     double s = slot[0];
 #pragma unroll
-    for (int i = 1; i < NT / 32; ++i) s = fmin(s, slot[2 * i]);
+    for (int i = 1; i < NT / 32; ++i) s = fmin(s, slot[4 * i]);
     buf ^= 1;
     return (int)s;
   }

@@ -306,6 +306,11 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   SP sp;
   sp.init(smem, spp);
   double* ring = ring_off >= 0 ? reinterpret_cast<double*>(smem + ring_off) : nullptr;
+  // near-history weights in shared memory (a runtime-indexed kernel-parameter
+  // array would be spilled to local memory)
+  __shared__ double s_anear[16];
+  if (threadIdx.x < 16) s_anear[threadIdx.x] = c.anear[threadIdx.x];
+  __syncthreads();
   Status st = {ST_OK, n, 0, -1, 0, 0, {0, 0}};
   double x[EPT];
 #pragma unroll
@@ -319,10 +324,12 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   }
   const double* hs = nullptr;
   int J = 0;
+  double hnext[EPT], cnext[EPT];  // this block's far rows, prefetched one substep ahead
   for (int r = 1; r <= c.m; ++r) {
     const double t = (double)n * c.dT + (double)(r - 1) * c.dt;
     const int rr = (r - 1) % HB;
     const int beta = (r - 1) / HB;
+    PF_T(10);
     if (rr == 0) {
       J = far_extent(beta);
       double* slot = scr + (size_t)(beta & 1) * 2 * HB * c.size;
@@ -334,6 +341,27 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         bracket_block<NT, EPT>(c, U, n, r, slot + (size_t)HB * c.size);
       }
       hs = slot;
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        const int e = threadIdx.x + i * NT;
+        hnext[i] = (e < c.size) ? __ldcg(hs + e) : 0.0;
+        cnext[i] = (e < c.size) ? __ldcg(hs + (size_t)HB * c.size + e) : 0.0;
+      }
+    }
+    PF_T(8);
+    double hcur[EPT], ccur[EPT];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      hcur[i] = hnext[i];
+      ccur[i] = cnext[i];
+    }
+    if (rr + 1 < HB) {  // issue next substep's far-row loads now; they land during this step
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) {
+        const int e = threadIdx.x + i * NT;
+        hnext[i] = (e < c.size) ? __ldcg(hs + (size_t)(rr + 1) * c.size + e) : 0.0;
+        cnext[i] = (e < c.size) ? __ldcg(hs + (size_t)(HB + rr + 1) * c.size + e) : 0.0;
+      }
     }
     const int p = r - 1 < EXO ? r - 1 : EXO;
     double h[EPT], ct[EPT], xg[EPT], xn[EPT];
@@ -342,12 +370,12 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       const int e = threadIdx.x + i * NT;
       double acc = 0.0, cb = 0.0, g = x[i];
       if (e < c.size) {
-        acc = __ldcg(hs + (size_t)rr * c.size + e);
+        acc = hcur[i];
         for (int j = J + 1; j < r; ++j) {
           const double v = ring ? ring[(size_t)(j & (NR - 1)) * c.size + e] : path[(size_t)j * c.size + e];
-          acc = fma(c.anear[r - j], v, acc);
+          acc = fma(s_anear[r - j], v, acc);
         }
-        cb = __ldcg(hs + (size_t)(HB + rr) * c.size + e);
+        cb = ccur[i];
         // extrapolated guess; row r-1 is x itself
         const double* w = kExtrap[p];
         g = w[0] * x[i];
@@ -361,6 +389,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       ct[i] = cb;
       xg[i] = g;
     }
+    PF_T(9);
     const int code = sp.step(c.fn, x, xg, t, c.gam_f, h, ct, xn, st);
     if (code != ST_OK) {
       st.code = code;

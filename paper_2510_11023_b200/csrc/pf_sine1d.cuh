@@ -133,11 +133,12 @@ struct Sine1D {
   cd *A, *B;
   double* dq;
   double2* xtab;  // {sin(pi x_q), sin(2 pi x_q)}
+  double* xq;     // x_q = (q + 1/2) / Q
   Reducer<NT> red;
   double tol2;
   int maxit;
 
-  static size_t smem_bytes() { return sizeof(cd) * (TW + 3 * Q) + sizeof(double) * (3 * Q + 128); }
+  static size_t smem_bytes() { return sizeof(cd) * (TW + 3 * Q) + sizeof(double) * (4 * Q + RED_DOUBLES); }
 
   __device__ void init(char* smem, const Sine1DParams& p) {
     cd* s = reinterpret_cast<cd*>(smem);
@@ -147,11 +148,14 @@ struct Sine1D {
     B = A + Q;
     dq = reinterpret_cast<double*>(B + Q);
     xtab = reinterpret_cast<double2*>(dq + Q);
-    red.init(reinterpret_cast<double*>(xtab + Q));
+    xq = reinterpret_cast<double*>(xtab + Q);
+    red.init(xq + Q);
     for (int j = threadIdx.x; j < TW; j += NT) tws[j] = p.twp[j];
     for (int j = threadIdx.x; j < Q; j += NT) {
       phs[j] = p.ph[j];
-      xtab[j] = fn_xtab(((double)j + 0.5) / (double)Q);
+      const double x = ((double)j + 0.5) / (double)Q;  // (arange(Q) + 0.5) / Q, as the oracle
+      xq[j] = x;
+      xtab[j] = fn_xtab(x);
     }
     twp = tws;
     ph = phs;
@@ -239,6 +243,7 @@ struct Sine1D {
   // only changes the iteration count, not the solution beyond pcg_tol).
   __device__ int step(const Fn& fn, const double* xprev, const double* xguess, double t, double gam,
                       const double* hist, const double* contrib, double* xout, Status& st) {
+    PF_T(0);
     // --- synthesis pair: u = S c_prev, v0 = S' x0 ------------------------
     {
       double av[EPT], bv[EPT];
@@ -252,6 +257,7 @@ struct Sine1D {
     bar<NT>();
     cd* R = fft_stockham<LG, NT, true>(A, B, twp);
     cd* O = (R == A) ? B : A;
+    PF_T(1);
     // --- pointwise coefficients (fused epilogue) ------------------------
     const double wq = 1.0 / (double)Q;
     const double emt = exp(-t);
@@ -265,8 +271,7 @@ struct Sine1D {
         const cd w = R[s];
         const double s1 = 0.5 * w.x, s2 = 0.5 * w.y;
         const double u = (q & 1) ? -s1 : s1;
-        const double xq = ((double)q + 0.5) / (double)Q;
-        const double Dv = fn_D(fn, xq, 0.0, t, u);
+        const double Dv = fn_D(fn, xq[q], 0.0, t, u);
         if (!isfinite(Dv)) {
           bad = min(bad, q);
           nbad += 1.0;
@@ -284,10 +289,12 @@ struct Sine1D {
       return ST_COEFF;
     }
     const double dbar = s01.x;
+    PF_T(2);
     // --- analysis pair: F = S^T g, K x0 = S'^T (d v0) --------------------
     cd* Z = fft_stockham<LG, NT, false>(R, O, twp);
+    PF_T(3);
     double x[EPT], r[EPT], p[EPT], z[EPT], pinv[EPT];
-    double bb = 0.0, rr = 0.0;
+    double bb = 0.0, rr = 0.0, rzl = 0.0;
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int k = mode(i);
@@ -304,12 +311,18 @@ struct Sine1D {
         r[i] = rhs - (x[i] + gam * kx);
         const double kk = (double)k;
         pinv[i] = 1.0 / (1.0 + gam * dbar * (CUDART_PI * CUDART_PI) * (kk * kk));
+        z[i] = pinv[i] * r[i];
+        p[i] = z[i];
         bb = fma(rhs, rhs, bb);
         rr = fma(r[i], r[i], rr);
+        rzl = fma(r[i], z[i], rzl);
       }
     }
-    const double2 s0 = red.sum2(bb, rr);
+    const double3 s0 = red.sum3(bb, rr, rzl);
+    PF_T(4);
     st.solves += 1;
+    // a non-finite right-hand side or guess fails here (SolverFailure, stepping.py:240-241)
+    if (!isfinite(s0.x) || !isfinite(s0.y)) return ST_SOLVER;
     if (s0.x == 0.0) {
 #pragma unroll
       for (int i = 0; i < EPT; ++i) xout[i] = 0.0;
@@ -319,17 +332,12 @@ struct Sine1D {
     double rrv = s0.y;
     int it = 0;
     if (rrv > thr) {
-      double rzl = 0.0;
-#pragma unroll
-      for (int i = 0; i < EPT; ++i) {
-        z[i] = pinv[i] * r[i];
-        p[i] = z[i];
-        rzl = fma(r[i], z[i], rzl);
-      }
-      double rz = red.sum(rzl);
+      double rz = s0.z;
       for (it = 1; it <= maxit; ++it) {
         double kp[EPT], qv[EPT];
+        PF_T(6);
         apply_k(p, kp);
+        PF_T(5);
         double pql = 0.0;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
@@ -338,6 +346,7 @@ struct Sine1D {
         }
         const double pq = red.sum(pql);
         const double alpha = rz / pq;
+        if (!isfinite(alpha)) return ST_SOLVER;
         double rrl = 0.0, rzn = 0.0;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
@@ -349,7 +358,8 @@ struct Sine1D {
         }
         const double2 s = red.sum2(rrl, rzn);
         rrv = s.x;
-        if (!(rrv > thr)) break;  // converged (NaN falls through to the check below)
+        if (!isfinite(rrv)) return ST_SOLVER;
+        if (!(rrv > thr)) break;  // converged
         const double beta = s.y / rz;
         rz = s.y;
 #pragma unroll
@@ -358,13 +368,10 @@ struct Sine1D {
       st.iters += (it > maxit) ? maxit : it;
       if (it > maxit) return ST_SOLVER;
     }
-    double nonfinite = 0.0;
+    // x = x0 + sum(alpha p) with finite alpha, p and a finite guess: finite
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      if (mode(i) <= M && !isfinite(x[i])) nonfinite = 1.0;
-      xout[i] = x[i];
-    }
-    if (red.sum(nonfinite) > 0.0) return ST_SOLVER;
+    for (int i = 0; i < EPT; ++i) xout[i] = x[i];
+    PF_T(7);
     return ST_OK;
   }
 };
