@@ -155,9 +155,8 @@ class Context:
             self._keep += [nodes, d1, qw]
             space = pf_space(1, int(op.degree), ptr(nodes), ptr(d1), ptr(qw), 0.0, 0)
         elif isinstance(op, SineOperator):
-            if op.dims != 1:
-                raise ValueError("the 2-D sine space is not built into this library yet")
-            space = pf_space(2, int(op.modes), None, None, None, float(op.pcg_tol), int(op.pcg_maxit))
+            space = pf_space(2 if op.dims == 1 else 3, int(op.modes), None, None, None, float(op.pcg_tol),
+                             int(op.pcg_maxit))
         else:
             raise ValueError(f"unsupported operator type {type(op).__name__}")
         wt = weights_for(alpha)

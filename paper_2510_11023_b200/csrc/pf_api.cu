@@ -21,6 +21,7 @@
 #include "pf_device.cuh"
 #include "pf_kernels.cuh"
 #include "pf_sine1d.cuh"
+#include "pf_sine2d.cuh"
 
 using pf::cd;
 using pf::Status;
@@ -50,6 +51,7 @@ struct DevBuf {
   }
 };
 
+struct Engine2D;  // 2-D sine engine (pf_engine2d.inc)
 }  // namespace
 
 struct pf_ctx {
@@ -85,7 +87,17 @@ struct pf_ctx {
   int num_sms = 0;
   int allow_helpers = 1;  // PF_NO_HELPERS=1 forces the inline far history
   int last_helpers = 0;
+  Engine2D* e2 = nullptr;  // PF_SPACE_SINE2D only
 };
+
+namespace {  // 2-D engine entry points (defined in pf_engine2d.inc)
+int e2_fine_sweep(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, int m, bool with_bracket,
+                  double* d_all = nullptr);
+int e2_coarse_step(pf_ctx* c, const double* d_H, int n, double* d_out);
+int e2_run_coarse(pf_ctx* c, double* d_traj);
+int e2_correct(pf_ctx* c, const double* ucur, const double* fold, const double* gold, double* gnew, double* unext,
+               int k, double* diff);
+}  // namespace
 
 namespace {
 
@@ -197,6 +209,7 @@ int ensure_status(pf_ctx* c, int n) {
 // When 2*bs CTAs fit on the device at once, launch cooperatively with one
 // helper CTA per slice (far history on otherwise idle SMs); else inline.
 int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, Status* d_st) {
+  if (c->kind == PF_SPACE_SINE2D) return e2_fine_sweep(c, d_u, n_lo, bs, d_out, c->grid.m, true);
   if (c->paths.ensure((size_t)bs * (c->grid.m + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "paths");
   if (c->scratch.ensure((size_t)bs * 4 * pf::HB * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
   if (c->sync_cap < bs) {
@@ -261,6 +274,7 @@ int launch_coarse(pf_ctx* c, const pf::CoarseArgs& a, Status* d_st) {
 // Decode a fine-sweep status array: the earliest substep r fails first;
 // at equal r a coefficient error precedes the solve (stepping.py:225-241).
 int decode_fine(pf_ctx* c, int n_lo, int count) {
+  if (c->kind == PF_SPACE_SINE2D) return 0;  // the 2-D engine reports synchronously
   PF_CUDA(c, cudaMemcpyAsync(c->h_status.data(), c->d_status, sizeof(Status) * count, cudaMemcpyDeviceToHost,
                              c->stream));
   PF_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -350,6 +364,8 @@ double l1_formula(double x, double alpha) {
 
 }  // namespace
 
+#include "pf_engine2d.inc"
+
 extern "C" {
 
 const char* pf_version(void) { return "parafrac_b200 0.1.0 (sm_100a)"; }
@@ -398,6 +414,17 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
     static const Variant by_lg[12] = {V_NONE, V_NONE, V_S2, V_S3, V_S4, V_S5, V_S6, V_S7, V_S8, V_S9, V_S10, V_S11};
     c->variant = by_lg[c->lgQ];
     c->smem = sizeof(cd) * (pf::tw_table_size(c->lgQ) + 3 * c->Q) + sizeof(double) * (4 * c->Q + pf::RED_DOUBLES);
+  } else if (space->kind == PF_SPACE_SINE2D) {
+    const int M = space->modes;
+    if (!is_pow2(M) || M < 4 || M > 256)
+      return set_error(c, PF_ERR_UNSUPPORTED, "2-D sine modes must be a power of two in [4, 256]");
+    c->M = M;
+    c->Q = 2 * M;
+    c->lgQ = 0;
+    while ((1 << c->lgQ) < c->Q) ++c->lgQ;
+    c->size = M * M;
+    c->variant = V_NONE;
+    c->smem = 0;
   } else if (space->kind == PF_SPACE_CHEB1D) {
     const int deg = space->modes;
     if (deg < 2) return set_error(c, PF_ERR_ARGUMENT, "degree must be at least 2 so interior nodes exist");
@@ -464,7 +491,7 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
   PF_CUDA(c, cudaMalloc(&c->d_afine, sizeof(double) * h_afine.size()));
   PF_CUDA(c, cudaMemcpy(c->d_afine, h_afine.data(), sizeof(double) * h_afine.size(), cudaMemcpyHostToDevice));
   PF_CUDA(c, cudaMemcpy(c->d_bfrac, c->h_bfrac.data(), sizeof(double) * need_frac, cudaMemcpyHostToDevice));
-  if (c->kind == PF_SPACE_SINE1D) {
+  if (c->kind == PF_SPACE_SINE1D || c->kind == PF_SPACE_SINE2D) {
     const int ntw = std::max(pf::tw_table_size(c->lgQ), 1);
     std::vector<cd> tw(ntw), ph(c->Q);
     const long double PI = 3.141592653589793238462643383279502884L;
@@ -502,6 +529,7 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
     PF_CUDA(c, cudaMemcpy(c->d_qw, c->h_qw.data(), sizeof(double) * c->npts, cudaMemcpyHostToDevice));
   }
   if (ensure_status(c, std::max(nt, 1))) return c->err.code;
+  if (c->kind == PF_SPACE_SINE2D && e2_init(c)) return c->err.code;
   c->err = pf_error{};
   return PF_OK;
 }
@@ -516,6 +544,7 @@ void pf_destroy(pf_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c->e2;
   delete c;
 }
 
@@ -615,6 +644,17 @@ int pf_coarse_step(pf_ctx* c, const double* history, int n_states, int step_inde
   cudaSetDevice(c->device);
   if (c->io.ensure((size_t)(n_states + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "io");
   if (upload(c, c->io.p, history, (size_t)n_states * c->size)) return c->err.code;
+  if (c->kind == PF_SPACE_SINE2D) {
+    double* d_out = c->io.p + (size_t)n_states * c->size;
+    int rc = e2_coarse_step(c, c->io.p, n, d_out);
+    if (rc) {
+      if (rc == PF_ERR_SOLVER || rc == PF_ERR_COEFFICIENT) c->err.step_n = step_index;
+      return rc;
+    }
+    if (download(c, out, d_out, c->size)) return c->err.code;
+    PF_CUDA(c, cudaStreamSynchronize(c->stream));
+    return 0;
+  }
   pf::CoarseArgs a{};
   a.mode = pf::CM_SINGLE;
   a.n_single = n;
@@ -629,6 +669,7 @@ int pf_coarse_step(pf_ctx* c, const double* history, int n_states, int step_inde
 }
 
 static int run_coarse_dev(pf_ctx* c, double* d_traj) {
+  if (c->kind == PF_SPACE_SINE2D) return e2_run_coarse(c, d_traj);
   pf::CoarseArgs a{};
   a.mode = pf::CM_RUN;
   a.traj = d_traj;
@@ -658,6 +699,7 @@ int pf_chain_fine(pf_ctx* c, const double* u0, double* traj) {
   if (c->io.ensure(rows * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "io");
   if (upload(c, c->io.p, u0, c->size)) return c->err.code;
   if (ensure_status(c, nt)) return c->err.code;
+  PF_CUDA(c, cudaMemsetAsync(c->d_status, 0, sizeof(Status) * nt, c->stream));
   for (int n = 0; n < nt; ++n) {
     int rc = launch_fine(c, c->io.p, n, 1, c->io.p + (size_t)(n + 1) * c->size, c->d_status + n);
     if (rc) return rc;
@@ -687,6 +729,24 @@ int pf_fine_sequential(pf_ctx* c, const double* u0, double* states) {
   cudaSetDevice(c->device);
   const long total = (long)c->grid.nt * c->grid.m;
   if (c->len_fine < total + 1) return set_error(c, PF_ERR_ARGUMENT, "weight table shorter than nt*m+1");
+  if (c->kind == PF_SPACE_SINE2D) {
+    // the full-history solver is one slice marched over nt*m substeps with no bracket
+    if (c->io.ensure((size_t)(total + 2) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "hist");
+    double* d_u0 = c->io.p;
+    double* d_all = c->io.p + c->size;
+    if (upload(c, d_u0, u0, c->size)) return c->err.code;
+    int rc = e2_fine_sweep(c, d_u0, 0, 1, nullptr, (int)total, false, d_all);
+    if (rc) {
+      c->err.step_n = c->err.step_r - 1;
+      c->err.step_r = -1;
+      return rc;
+    }
+    for (int n = 0; n <= c->grid.nt; ++n)
+      if (download(c, states + (size_t)n * c->size, d_all + (size_t)n * c->grid.m * c->size, c->size))
+        return c->err.code;
+    PF_CUDA(c, cudaStreamSynchronize(c->stream));
+    return 0;
+  }
   if (c->paths.ensure((size_t)(total + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "hist");
   if (upload(c, c->paths.p, u0, c->size)) return c->err.code;
   pf::Common cm = make_common(c);
@@ -743,6 +803,14 @@ int pf_dev_parareal_correct(pf_ctx* c, const double* d_fold, int k, double* diff
   if (d_fold && d_fold != c->fold.p)
     PF_CUDA(c, cudaMemcpyAsync(c->fold.p, d_fold, (size_t)c->grid.nt * c->size * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   float ms = 0.f;
+  if (c->kind == PF_SPACE_SINE2D) {
+    double h2 = 0.0;
+    int rc2 = e2_correct(c, c->U.p, c->fold.p, c->gold.p, c->gnew.p, c->Unext.p, k, &h2);
+    if (rc2) return rc2;
+    if (diff) *diff = h2;
+    std::swap(c->U, c->Unext);
+    return 0;
+  }
   PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
   int rc = launch_coarse(c, a, c->d_status);
   if (rc) return rc;

@@ -1,0 +1,785 @@
+// Sine spectral-Galerkin space, 2-D tensor basis, matrix-free.
+//
+// State C[k1][k2] (M x M, k1 = x mode) of phi = 2 sin(k1 pi x) sin(k2 pi y) on
+// the Q x Q midpoint grid (Q = 2M), W = 1/Q^2.  Per substep, for every system
+// b of a batch (all slices of a sweep, or one coarse step):
+//
+//   (I + gam K) C = (hist + gam F) + contrib,    K = K(U_prev), F = F(U_prev)
+//   K C = S'1^T (W d (S'1 C S2^T)) S2 + S1^T (W d (S1 C S'2^T)) S'2
+//
+// solved by PCG (preconditioner 1/(1 + gam dbar pi^2 (k1^2 + k2^2)), dbar =
+// sum W d, initial guess = order-5 extrapolation of the slice path), the same
+// recurrence the oracle (oracle.Sine2D) runs.  One application of K is four
+// batched line passes over all systems, each a DCT pair as one complex FFT:
+//
+//   rows   (along y):  C[k1][.]   -> Hs[q2][k1] = S2 C,   Hc[q2][k1] = S'2 C
+//   cols   (along x):  Hs, Hc     -> Gx = S'1 Hs, Gy = S1 Hc -> Yx = W d Gx, Yy = W d Gy
+//                                 -> Ax = S'1^T Yx, Ay = S1^T Yy           (fused)
+//   rows   (along y):  Ax, Ay     -> K C = Ax S2 + Ay S'2
+//
+// Line tiles are staged through shared memory so every global access is a
+// contiguous run (the [q2][k1] layouts hold the x-lines contiguous, the row
+// passes read TL consecutive k1 per q2).  The per-system scalars (dbar, the CG
+// dots, alpha, beta, convergence) are reduced by one warp per system in a
+// fixed order: results are deterministic and independent of the batch split.
+#pragma once
+#include "pf_device.cuh"
+#include "pf_sine1d.cuh"
+
+namespace pf {
+
+// Stockham FFT over TL independent lines per CTA (lane = thread index within
+// the line), CTA-wide barriers; same arithmetic as fft_stockham.
+template <int LG, int TPL, bool INV>
+__device__ __forceinline__ cd* fft_lines(cd* a, cd* b, const cd* __restrict__ twp, int lane) {
+  constexpr int L = 1 << LG;
+  constexpr int L4 = L >> 2;
+  int off = 0;
+#pragma unroll
+  for (int pass = 0; pass < LG / 2; ++pass) {
+    const int Ns = 1 << (2 * pass);
+#pragma unroll
+    for (int j0 = 0; j0 < L4; j0 += TPL) {
+      const int j = j0 + lane;
+      if (L4 % TPL == 0 || j < L4) {
+        const int k = j & (Ns - 1);
+        cd v0 = a[sw(j)], v1 = a[sw(j + L4)], v2 = a[sw(j + 2 * L4)], v3 = a[sw(j + 3 * L4)];
+        if (pass > 0) {
+          cd w1 = twp[off + k], w2 = twp[off + Ns + k], w3 = twp[off + 2 * Ns + k];
+          if (INV) {
+            w1.y = -w1.y;
+            w2.y = -w2.y;
+            w3.y = -w3.y;
+          }
+          v1 = cmul(v1, w1);
+          v2 = cmul(v2, w2);
+          v3 = cmul(v3, w3);
+        }
+        const cd t0 = cadd(v0, v2), t1 = csub(v0, v2), t2 = cadd(v1, v3), t3 = csub(v1, v3);
+        const cd mi3 = {t3.y, -t3.x};
+        const int base = ((j - k) << 2) + k;
+        b[sw(base)] = cadd(t0, t2);
+        b[sw(base + Ns)] = INV ? csub(t1, mi3) : cadd(t1, mi3);
+        b[sw(base + 2 * Ns)] = csub(t0, t2);
+        b[sw(base + 3 * Ns)] = INV ? cadd(t1, mi3) : csub(t1, mi3);
+      }
+    }
+    if (pass > 0) off += 3 * Ns;
+    __syncthreads();
+    cd* t = a;
+    a = b;
+    b = t;
+  }
+  if (LG & 1) {
+    constexpr int L2 = L >> 1;
+    constexpr int Ns = 1 << (LG - 1);
+#pragma unroll
+    for (int j0 = 0; j0 < L2; j0 += TPL) {
+      const int j = j0 + lane;
+      if (L2 % TPL == 0 || j < L2) {
+        const int k = j & (Ns - 1);
+        cd v0 = a[sw(j)], v1 = a[sw(j + L2)];
+        if (Ns > 1) {
+          cd w = twp[off + k];
+          if (INV) w.y = -w.y;
+          v1 = cmul(v1, w);
+        }
+        const int base = ((j - k) << 1) + k;
+        b[sw(base)] = cadd(v0, v1);
+        b[sw(base + Ns)] = csub(v0, v1);
+      }
+    }
+    __syncthreads();
+    cd* t = a;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+struct Sine2DArgs {
+  Fn fn;
+  int M, Q, B;              // modes per axis, grid per axis, systems in the batch
+  const cd* twp;            // per-pass twiddles (length-Q FFT)
+  const cd* ph;             // exp(i pi j / 2Q)
+  const double* xq;         // midpoints (q+1/2)/Q
+  // per-system times t_b = (n0 + b) * dTs + tr  (fine: dTs = dT, tr = (r-1) dt)
+  int n0;
+  double dTs, tr, gam, tol2;
+  // mode-space arrays: pointer + stride (doubles) between systems
+  const double* Cp; long sCp;   // state at the previous substep
+  const double* X0; long sX0;   // PCG initial guess
+  const double* HIST; long sH;  // L1 history term
+  const double* CON; long sC;   // coarse bracket (nullptr: zero)
+  double* X; long sX;           // solution (written in place)
+  double *R, *Z, *P, *QV, *PINV;  // (B, M*M) work
+  // line arrays (B, Q, M): y-transformed, x-modes
+  double *Hu, *Hs, *Hc, *Ag, *Ax, *Ay;
+  double* D;                    // (B, Q, Q) W*d on the grid [q2][q1]
+  double* part;                 // (B, Q, 4) per-line partial sums
+  double* sc;                   // (B, 16) per-system scalars
+  int* bad;                     // (B) smallest non-finite grid index (INT_MAX none)
+};
+
+// per-system scalar slots
+enum { S_DBAR = 0, S_BB, S_RR, S_RZ, S_PQ, S_ALPHA, S_BETA, S_THR, S_DONE, S_ZERO, S_IT, S_FAIL };
+
+template <int LG>
+struct Line2D {
+  static constexpr int Q = 1 << LG, M = Q / 2, TPL = (Q / 4 < 256 ? Q / 4 : 256), NT = 256,
+                       TL = (NT / TPL) > 0 ? NT / TPL : 1;
+  static constexpr int TW = tw_table_size(LG);
+  static constexpr double SQ2 = 1.4142135623730951;
+  static size_t smem_bytes() { return sizeof(cd) * (TW + Q + 2 * TL * Q) + sizeof(double) * TL * (Q + 1); }
+};
+
+// Load the shared tables, carve the per-line double buffers.
+template <int LG>
+__device__ __forceinline__ void line_setup(char* smem, const Sine2DArgs& a, cd*& twp, cd*& ph, cd*& A, cd*& B,
+                                           double*& stage) {
+  using L = Line2D<LG>;
+  cd* s = reinterpret_cast<cd*>(smem);
+  twp = s;
+  ph = s + L::TW;
+  A = ph + L::Q;
+  B = A + L::TL * L::Q;
+  stage = reinterpret_cast<double*>(B + L::TL * L::Q);
+  for (int j = threadIdx.x; j < L::TW; j += L::NT) twp[j] = a.twp[j];
+  for (int j = threadIdx.x; j < L::Q; j += L::NT) ph[j] = a.ph[j];
+  __syncthreads();  // tables are read by every line before the first FFT barrier
+}
+
+// synthesis-pair FFT input for one line from mode values av (sin) / bv (cos),
+// k = 1..M (mode of lane-owned index).  Writes W_k and W_{Q-k}.
+template <int LG>
+__device__ __forceinline__ void synth_write(cd* W, const cd* ph, int k, double av, double bv) {
+  constexpr int Q = 1 << LG, M = Q / 2;
+  if (k < M) {
+    const cd p = ph[k], pq = ph[Q - k];
+    const cd v1 = {p.y * av, -p.x * av};
+    const cd v2 = {p.x * bv, p.y * bv};
+    W[sw(k)] = {v1.x - v2.y, v1.y + v2.x};
+    const cd u1 = {pq.x * av, pq.y * av};
+    const cd u2 = {pq.y * bv, -pq.x * bv};
+    W[sw(Q - k)] = {u1.x - u2.y, u1.y + u2.x};
+  } else {
+    const cd p = ph[M];
+    const cd v1 = {p.x * av + p.y * av, p.y * av - p.x * av};
+    const cd v2 = {p.x * bv + p.y * bv, p.y * bv - p.x * bv};
+    W[sw(M)] = {v1.x - v2.y, v1.y + v2.x};
+  }
+}
+
+// analysis post-processing for mode k: X1 = sum g sin, X2 = sum y cos
+__device__ __forceinline__ double2 anal_read(const cd* Z, const cd* ph, int Q, int k) {
+  const cd a = Z[sw(k)], b = Z[sw(Q - k)], c = ph[k], c2 = ph[Q - k];
+  const double Dx = a.x - b.x, Dy = a.y + b.y;
+  return make_double2(0.5 * (c2.x * (b.x + a.x) + c2.y * (b.y - a.y)), 0.5 * (c.x * Dy - c.y * Dx));
+}
+
+// ---------------------------------------------------------------------------
+// row synthesis (along y): lines k1 of the mode arrays -> H[q2][k1]
+// SETUP: FFT1 (a = sqrt2 Cp, b = sqrt2 pi k2 X0) -> Hu (sin), Hc (cos);
+//        FFT2 (a = sqrt2 X0)                    -> Hs (sin)
+// CG:    p = z + beta p, then FFT (a = sqrt2 p, b = sqrt2 pi k2 p) -> Hs, Hc
+// ---------------------------------------------------------------------------
+template <int LG, bool SETUP>
+__global__ void __launch_bounds__(256) k2_rows_syn(Sine2DArgs a) {
+  using L = Line2D<LG>;
+  extern __shared__ __align__(16) char smem[];
+  const int b = blockIdx.y;
+  if (!SETUP && a.sc[b * 16 + S_DONE] != 0.0) return;
+  cd *twp, *ph, *A, *B;
+  double* stage;
+  line_setup<LG>(smem, a, twp, ph, A, B, stage);
+  const int line = threadIdx.x / L::TPL, lane = threadIdx.x % L::TPL;
+  const int k1 = blockIdx.x * L::TL + line + 1;  // x mode of this line
+  const bool live = line < L::TL && k1 <= L::M;
+  cd* W = A + line * L::Q;
+  const size_t row = (size_t)(k1 - 1) * L::M;
+  const double beta = SETUP ? 0.0 : a.sc[b * 16 + S_BETA];
+  constexpr int NF = SETUP ? 2 : 1;
+  for (int f = 0; f < NF; ++f) {
+    if (live) {
+      if (lane == 0) W[0] = {0.0, 0.0};
+      for (int k = lane + 1; k <= L::M; k += L::TPL) {
+        double av, bv;
+        if (SETUP) {
+          const double x0 = a.X0[b * a.sX0 + row + k - 1];
+          if (f == 0) {
+            av = L::SQ2 * a.Cp[b * a.sCp + row + k - 1];
+            bv = L::SQ2 * CUDART_PI * (double)k * x0;
+          } else {
+            av = L::SQ2 * x0;
+            bv = 0.0;
+          }
+        } else {
+          double* pp = a.P + (size_t)b * L::M * L::M + row + k - 1;
+          const double pn = fma(beta, *pp, a.Z[(size_t)b * L::M * L::M + row + k - 1]);
+          *pp = pn;
+          av = L::SQ2 * pn;
+          bv = L::SQ2 * CUDART_PI * (double)k * pn;
+        }
+        synth_write<LG>(W, ph, k, av, bv);
+      }
+    }
+    __syncthreads();
+    cd* Rl = fft_lines<LG, L::TPL, true>(A + line * L::Q, B + line * L::Q, twp, lane);
+    // stage s (sin) and c (cos) per line, then write [q2][k1] tiles
+    double* s_sin = stage;  // TL * (Q+1)  (reused for both outputs in two rounds)
+    for (int out = 0; out < 2; ++out) {
+      if (live)
+        for (int q = lane; q < L::Q; q += L::TPL) {
+          const int idx = (q & 1) ? (L::Q - 1 - (q >> 1)) : (q >> 1);
+          const cd w = Rl[sw(idx)];
+          s_sin[line * (L::Q + 1) + q] = out == 0 ? ((q & 1) ? -0.5 * w.x : 0.5 * w.x) : 0.5 * w.y;
+        }
+      __syncthreads();
+      double* dst = SETUP ? (f == 0 ? (out == 0 ? a.Hu : a.Hc) : (out == 0 ? a.Hs : nullptr))
+                          : (out == 0 ? a.Hs : a.Hc);
+      if (dst) {
+        const int k1b = blockIdx.x * L::TL;  // first k1-1 of the tile
+        for (int e = threadIdx.x; e < L::TL * L::Q; e += L::NT) {
+          const int q2 = e / L::TL, l = e % L::TL;
+          if (k1b + l < L::M) dst[((size_t)b * L::Q + q2) * L::M + k1b + l] = s_sin[l * (L::Q + 1) + q2];
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// column pass (along x) for lines q2: synthesis pair, pointwise, analysis pair
+// SETUP: FFT1 (a = sqrt2 Hu, b = sqrt2 pi k1 Hs) -> U (sin), Gx (cos)
+//        FFT2 (a = sqrt2 Hc)                    -> Gy (sin)
+//        d = W D, g = W f, Yx = d Gx, Yy = d Gy; store d; line partial sum d
+//        FFT3 (g -> sin, Yx -> cos) -> Ag = sqrt2 X1, Ax = sqrt2 pi k1 X2
+//        FFT4 (Yy -> sin)           -> Ay = sqrt2 X1
+// CG:    FFT1 (a = sqrt2 Hc, b = sqrt2 pi k1 Hs) -> Gy (sin), Gx (cos)
+//        Yx = d Gx, Yy = d Gy; FFT2 (Yy -> sin, Yx -> cos) -> Ay, Ax
+// ---------------------------------------------------------------------------
+template <int LG, bool SETUP>
+__global__ void __launch_bounds__(256) k2_cols(Sine2DArgs a) {
+  using L = Line2D<LG>;
+  extern __shared__ __align__(16) char smem[];
+  const int b = blockIdx.y;
+  if (!SETUP && a.sc[b * 16 + S_DONE] != 0.0) return;
+  cd *twp, *ph, *A, *B;
+  double* stage;
+  line_setup<LG>(smem, a, twp, ph, A, B, stage);
+  const int line = threadIdx.x / L::TPL, lane = threadIdx.x % L::TPL;
+  const int q2 = blockIdx.x * L::TL + line;
+  const bool live = line < L::TL && q2 < L::Q;
+  const size_t hl = ((size_t)b * L::Q + q2) * L::M;  // H line base [b][q2][.]
+  const size_t gl = ((size_t)b * L::Q + q2) * L::Q;  // grid line base [b][q2][.]
+  const double wq = 1.0 / ((double)L::Q * (double)L::Q);
+  const double t = (double)(a.n0 + b) * a.dTs + a.tr;
+  const double emt = exp(-t);
+  // grid values kept in registers between the synthesis and analysis FFTs
+  constexpr int QPL = (L::Q + L::TPL - 1) / L::TPL;
+  double gx[QPL], gy[QPL], uu[QPL];
+  double dsum = 0.0;
+  int bad = 0x7fffffff;
+  const int nsyn = SETUP ? 2 : 1;
+  for (int f = 0; f < nsyn; ++f) {
+    cd* W = A + line * L::Q;
+    if (live) {
+      if (lane == 0) W[0] = {0.0, 0.0};
+      for (int k = lane + 1; k <= L::M; k += L::TPL) {
+        double av, bv;
+        if (SETUP && f == 0) {
+          av = L::SQ2 * a.Hu[hl + k - 1];
+          bv = L::SQ2 * CUDART_PI * (double)k * a.Hs[hl + k - 1];
+        } else if (SETUP) {
+          av = L::SQ2 * a.Hc[hl + k - 1];
+          bv = 0.0;
+        } else {
+          av = L::SQ2 * a.Hc[hl + k - 1];
+          bv = L::SQ2 * CUDART_PI * (double)k * a.Hs[hl + k - 1];
+        }
+        synth_write<LG>(W, ph, k, av, bv);
+      }
+    }
+    __syncthreads();
+    cd* Rl = fft_lines<LG, L::TPL, true>(A + line * L::Q, B + line * L::Q, twp, lane);
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < QPL; ++i) {
+        const int q = lane + i * L::TPL;
+        if (q < L::Q) {
+          const int idx = (q & 1) ? (L::Q - 1 - (q >> 1)) : (q >> 1);
+          const cd w = Rl[sw(idx)];
+          const double s = (q & 1) ? -0.5 * w.x : 0.5 * w.x, c = 0.5 * w.y;
+          if (SETUP && f == 0) {
+            uu[i] = s;
+            gx[i] = c;
+          } else if (SETUP) {
+            gy[i] = s;
+          } else {
+            gy[i] = s;
+            gx[i] = c;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // pointwise (and, in SETUP, the coefficient evaluation) -> analysis inputs
+  const int nana = SETUP ? 2 : 1;
+  for (int f = 0; f < nana; ++f) {
+    cd* Wz = A + line * L::Q;
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < QPL; ++i) {
+        const int q1 = lane + i * L::TPL;
+        if (q1 < L::Q) {
+          double d, g = 0.0;
+          if (SETUP) {
+            if (f == 0) {
+              const double x1 = a.xq[q1];
+              const double Dv = fn_D(a.fn, x1, a.xq[q2], t, uu[i]);
+              if (!isfinite(Dv)) bad = min(bad, q2 * L::Q + q1);
+              d = wq * Dv;
+              g = wq * (a.fn.id == 4 ? fn_f(a.fn, make_double2(0.0, 0.0), emt, uu[i])
+                                     : fn_f(a.fn, fn_xtab(x1), emt, uu[i]));
+              a.D[gl + q1] = d;
+              dsum += d;
+              uu[i] = d;  // keep d for the second analysis FFT
+            } else {
+              d = uu[i];
+            }
+          } else {
+            d = a.D[gl + q1];
+          }
+          const int idx = (q1 & 1) ? (L::Q - 1 - (q1 >> 1)) : (q1 >> 1);
+          // analysis pair input: sin part (g or Yy), cos part (Yx)
+          double sp, cp;
+          if (SETUP) {
+            sp = f == 0 ? g : d * gy[i];
+            cp = f == 0 ? d * gx[i] : 0.0;
+          } else {
+            sp = d * gy[i];
+            cp = d * gx[i];
+          }
+          Wz[sw(idx)] = {(q1 & 1) ? -sp : sp, cp};
+        }
+      }
+    }
+    __syncthreads();
+    cd* Zl = fft_lines<LG, L::TPL, false>(A + line * L::Q, B + line * L::Q, twp, lane);
+    if (live) {
+      for (int k = lane + 1; k <= L::M; k += L::TPL) {
+        const double2 X = anal_read(Zl, ph, L::Q, k);
+        if (SETUP) {
+          if (f == 0) {
+            a.Ag[hl + k - 1] = L::SQ2 * X.x;
+            a.Ax[hl + k - 1] = L::SQ2 * CUDART_PI * (double)k * X.y;
+          } else {
+            a.Ay[hl + k - 1] = L::SQ2 * X.x;
+          }
+        } else {
+          a.Ay[hl + k - 1] = L::SQ2 * X.x;
+          a.Ax[hl + k - 1] = L::SQ2 * CUDART_PI * (double)k * X.y;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (SETUP) {
+    // per-line partial of dbar (fixed order: lane-strided, then shuffle within the line's warps)
+    double* red = stage;  // TL * TPL doubles
+    red[threadIdx.x] = live ? dsum : 0.0;
+    __syncthreads();
+    if (live && lane == 0) {
+      double s = 0.0;
+      for (int i = 0; i < L::TPL; ++i) s += red[line * L::TPL + i];
+      a.part[((size_t)b * L::Q + q2) * 4 + 0] = s;
+    }
+    if (bad != 0x7fffffff) atomicMin(a.bad + b, bad);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// row analysis (along y) for lines k1, reading the [q2][k1] arrays
+// SETUP: FFT1 (Ag -> sin, Ay -> cos), FFT2 (Ax -> sin) ->
+//        F = sqrt2 X1(Ag), K x0 = sqrt2 X1(Ax) + sqrt2 pi k2 X2(Ay);
+//        rhs, r0, z0, p0 = z0, x = x0, pinv; line partials (bb, rr, rz)
+// CG:    FFT1 (Ax -> sin, Ay -> cos) -> Kp; q = p + gam Kp; line partial pq
+// ---------------------------------------------------------------------------
+template <int LG, bool SETUP>
+__global__ void __launch_bounds__(256) k2_rows_ana(Sine2DArgs a) {
+  using L = Line2D<LG>;
+  extern __shared__ __align__(16) char smem[];
+  const int b = blockIdx.y;
+  if (!SETUP && a.sc[b * 16 + S_DONE] != 0.0) return;
+  cd *twp, *ph, *A, *B;
+  double* stage;
+  line_setup<LG>(smem, a, twp, ph, A, B, stage);
+  const int line = threadIdx.x / L::TPL, lane = threadIdx.x % L::TPL;
+  const int k1b = blockIdx.x * L::TL;
+  const int k1 = k1b + line + 1;
+  const bool live = line < L::TL && k1 <= L::M;
+  const size_t MM = (size_t)L::M * L::M;
+  const size_t row = (size_t)(k1 - 1) * L::M;
+  double kv[(L::M + L::TPL - 1) / L::TPL];  // K applied to the line's modes
+  double fv[(L::M + L::TPL - 1) / L::TPL];
+  constexpr int MPL = (L::M + L::TPL - 1) / L::TPL;
+#pragma unroll
+  for (int i = 0; i < MPL; ++i) kv[i] = fv[i] = 0.0;
+  const int nf = SETUP ? 2 : 1;
+  for (int f = 0; f < nf; ++f) {
+    // stage the tile's columns: src[q2][k1b .. k1b+TL) -> stage[l][q2]
+    const double* s1 = SETUP ? (f == 0 ? a.Ag : a.Ax) : a.Ax;
+    const double* s2 = SETUP ? (f == 0 ? a.Ay : nullptr) : a.Ay;
+    for (int e = threadIdx.x; e < L::TL * L::Q; e += L::NT) {
+      const int q2 = e / L::TL, l = e % L::TL;
+      if (k1b + l < L::M) {
+        const size_t o = ((size_t)b * L::Q + q2) * L::M + k1b + l;
+        const double g = s1[o], y = s2 ? s2[o] : 0.0;
+        const int idx = (q2 & 1) ? (L::Q - 1 - (q2 >> 1)) : (q2 >> 1);
+        A[l * L::Q + sw(idx)] = {(q2 & 1) ? -g : g, y};
+      }
+    }
+    __syncthreads();
+    cd* Zl = fft_lines<LG, L::TPL, false>(A + line * L::Q, B + line * L::Q, twp, lane);
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < MPL; ++i) {
+        const int k2 = lane + 1 + i * L::TPL;
+        if (k2 <= L::M) {
+          const double2 X = anal_read(Zl, ph, L::Q, k2);
+          if (SETUP && f == 0) {
+            fv[i] = L::SQ2 * X.x;                                // F
+            kv[i] = L::SQ2 * CUDART_PI * (double)k2 * X.y;       // Ay S'2 part
+          } else if (SETUP) {
+            kv[i] += L::SQ2 * X.x;                               // Ax S2 part
+          } else {
+            kv[i] = L::SQ2 * X.x + L::SQ2 * CUDART_PI * (double)k2 * X.y;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+  if (live) {
+    const double gam = a.gam;
+    if (SETUP) {
+      const double dbar = a.sc[b * 16 + S_DBAR];
+#pragma unroll
+      for (int i = 0; i < MPL; ++i) {
+        const int k2 = lane + 1 + i * L::TPL;
+        if (k2 <= L::M) {
+          const size_t e = row + k2 - 1;
+          const double hist = a.HIST[b * a.sH + e];
+          const double con = a.CON ? a.CON[b * a.sC + e] : 0.0;
+          const double rhs = __dadd_rn(__dadd_rn(hist, __dmul_rn(gam, fv[i])), con);
+          const double x0 = a.X0[b * a.sX0 + e];
+          const double r = rhs - (x0 + gam * kv[i]);
+          const double kk = (double)k1 * (double)k1 + (double)k2 * (double)k2;
+          const double pinv = 1.0 / (1.0 + gam * dbar * (CUDART_PI * CUDART_PI) * kk);
+          const double z = pinv * r;
+          a.X[b * a.sX + e] = x0;
+          a.R[b * MM + e] = r;
+          a.Z[b * MM + e] = z;
+          a.P[b * MM + e] = z;
+          a.PINV[b * MM + e] = pinv;
+          p0 = fma(rhs, rhs, p0);
+          p1 = fma(r, r, p1);
+          p2 = fma(r, z, p2);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < MPL; ++i) {
+        const int k2 = lane + 1 + i * L::TPL;
+        if (k2 <= L::M) {
+          const size_t e = row + k2 - 1;
+          const double p = a.P[b * MM + e];
+          const double qv = p + gam * kv[i];
+          a.QV[b * MM + e] = qv;
+          p0 = fma(p, qv, p0);
+        }
+      }
+    }
+  }
+  // line partials in fixed order
+  double* red = reinterpret_cast<double*>(stage);
+  red[3 * threadIdx.x] = p0;
+  red[3 * threadIdx.x + 1] = p1;
+  red[3 * threadIdx.x + 2] = p2;
+  __syncthreads();
+  if (live && lane == 0) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int i = 0; i < L::TPL; ++i) {
+      s0 += red[3 * (line * L::TPL + i)];
+      s1 += red[3 * (line * L::TPL + i) + 1];
+      s2 += red[3 * (line * L::TPL + i) + 2];
+    }
+    double* pp = a.part + ((size_t)b * L::Q + (k1 - 1)) * 4;
+    pp[1] = s0;
+    pp[2] = s1;
+    pp[3] = s2;
+  }
+}
+
+// CG vector update over modes: x += alpha p, r -= alpha q, z = pinv r; line partials (rr, rz)
+template <int LG>
+__global__ void __launch_bounds__(256) k2_update(Sine2DArgs a) {
+  using L = Line2D<LG>;
+  const int b = blockIdx.y;
+  if (a.sc[b * 16 + S_DONE] != 0.0) return;
+  const double alpha = a.sc[b * 16 + S_ALPHA];
+  const size_t MM = (size_t)L::M * L::M;
+  __shared__ double red[2 * 256];
+  // one CTA per (k1 tile of 256/M... ) : threads over modes of TLU rows
+  constexpr int TLU = (256 / L::M) > 0 ? 256 / L::M : 1;
+  const int k1 = blockIdx.x * TLU + (int)threadIdx.x / (L::M < 256 ? L::M : 256);
+  double rr = 0.0, rz = 0.0;
+  if (k1 < L::M) {
+    for (int k2 = threadIdx.x % (L::M < 256 ? L::M : 256); k2 < L::M; k2 += (L::M < 256 ? L::M : 256)) {
+      const size_t e = (size_t)k1 * L::M + k2;
+      double* x = a.X + b * a.sX + e;
+      *x = fma(alpha, a.P[b * MM + e], *x);
+      const double r = fma(-alpha, a.QV[b * MM + e], a.R[b * MM + e]);
+      const double z = a.PINV[b * MM + e] * r;
+      a.R[b * MM + e] = r;
+      a.Z[b * MM + e] = z;
+      rr = fma(r, r, rr);
+      rz = fma(r, z, rz);
+    }
+  }
+  red[2 * threadIdx.x] = rr;
+  red[2 * threadIdx.x + 1] = rz;
+  __syncthreads();
+  constexpr int TPR = (L::M < 256 ? L::M : 256);
+  if (k1 < L::M && threadIdx.x % TPR == 0) {
+    double s0 = 0.0, s1 = 0.0;
+    const int base = (threadIdx.x / TPR) * TPR;
+    for (int i = 0; i < TPR; ++i) {
+      s0 += red[2 * (base + i)];
+      s1 += red[2 * (base + i) + 1];
+    }
+    double* pp = a.part + ((size_t)b * L::Q + k1) * 4;
+    pp[2] = s0;
+    pp[3] = s1;
+  }
+}
+
+// Per-system scalar reductions: one warp per system sums the M line
+// partials in a fixed order.  kind 0: after SETUP (bb, rr, rz); 1: pq -> alpha;
+// 2: (rr, rz) -> convergence / beta.  Writes the count of unfinished systems.
+__global__ void k2_reduce(Sine2DArgs a, int kind, int maxit, int* remaining) {
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x;
+  if (kind == 3) {  // dbar = sum over the Q column partials
+    double s = 0.0;
+    for (int q = lane; q < a.Q; q += 32) s += a.part[((size_t)b * a.Q + q) * 4];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) a.sc[b * 16 + S_DBAR] = s;
+    return;
+  }
+  double s[3] = {0.0, 0.0, 0.0};
+  const int slot0 = kind == 1 ? 1 : (kind == 0 ? 1 : 2);
+  const int nval = kind == 0 ? 3 : (kind == 1 ? 1 : 2);
+  if (a.sc[b * 16 + S_DONE] != 0.0 && kind != 0) {
+    return;
+  }
+  for (int k = lane; k < a.M; k += 32)
+    for (int v = 0; v < nval; ++v) s[v] += a.part[((size_t)b * a.Q + k) * 4 + slot0 + v];
+  for (int v = 0; v < 3; ++v)
+    for (int o = 16; o > 0; o >>= 1) s[v] += __shfl_xor_sync(0xffffffffu, s[v], o);
+  if (lane != 0) return;
+  double* sc = a.sc + b * 16;
+  if (kind == 0) {
+    sc[S_BB] = s[0];
+    sc[S_RR] = s[1];
+    sc[S_RZ] = s[2];
+    sc[S_IT] = 0.0;
+    sc[S_BETA] = 0.0;  // first direction p = z
+    sc[S_THR] = a.tol2 * s[0];
+    sc[S_FAIL] = (!isfinite(s[0]) || !isfinite(s[1])) ? 1.0 : 0.0;
+    sc[S_ZERO] = (s[0] == 0.0) ? 1.0 : 0.0;
+    sc[S_DONE] = (sc[S_FAIL] != 0.0 || s[0] == 0.0 || !(s[1] > sc[S_THR])) ? 1.0 : 0.0;
+  } else if (kind == 1) {
+    const double alpha = sc[S_RZ] / s[0];
+    sc[S_ALPHA] = alpha;
+    if (!isfinite(alpha)) {
+      sc[S_FAIL] = 1.0;
+      sc[S_DONE] = 1.0;
+    }
+  } else {
+    sc[S_IT] += 1.0;
+    if (!isfinite(s[0])) {
+      sc[S_FAIL] = 1.0;
+      sc[S_DONE] = 1.0;
+    } else if (!(s[0] > sc[S_THR])) {
+      sc[S_DONE] = 1.0;
+    } else if (sc[S_IT] >= (double)maxit) {
+      sc[S_FAIL] = 2.0;
+      sc[S_DONE] = 1.0;
+    } else {
+      sc[S_BETA] = s[1] / sc[S_RZ];
+      sc[S_RZ] = s[1];
+    }
+  }
+  if (sc[S_DONE] == 0.0) atomicAdd(remaining, 1);
+}
+
+// zero right-hand side: the solution is zero (stepping's solve of (I+gam K) x = 0)
+__global__ void k2_zero_fix(Sine2DArgs a) {
+  const int b = blockIdx.y;
+  if (a.sc[b * 16 + S_ZERO] == 0.0) return;
+  const size_t MM = (size_t)a.M * a.M;
+  for (size_t e = blockIdx.x * blockDim.x + threadIdx.x; e < MM; e += (size_t)gridDim.x * blockDim.x)
+    a.X[b * a.sX + e] = 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// history for batched slices (2-D): same blocked Toeplitz GEMM as 1-D, tiled
+// over modes.  far[b][rr][e] (HB rows) and bracket rows for block beta.
+// ---------------------------------------------------------------------------
+struct Hist2DArgs {
+  int MM, m, n0;
+  const double* bfine;
+  const double* afine;
+  const double* bfrac;
+  double minv;
+  const double* U;       // coarse states (nt+1, MM)
+  const double* paths;   // (B, m+1, MM)
+  double* far;           // (B, 2, HB, MM): [b][0] far history, [b][1] bracket
+};
+
+template <int NT, int EPT>
+__global__ void __launch_bounds__(NT) k2_far(Hist2DArgs h, int beta) {
+  const int b = blockIdx.y;
+  const int n = h.n0 + b;
+  const int e0 = blockIdx.x * NT * EPT;
+  const size_t MM = h.MM;
+  const int R0 = beta * HB;
+  const int J = (beta > 0 ? beta - 1 : 0) * HB;
+  const double* path = h.paths + (size_t)b * (h.m + 1) * MM;
+  double acc[HB][EPT], cb[HB][EPT];
+  double c0[EPT];
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int e = e0 + threadIdx.x + i * NT;
+    c0[i] = (e < h.MM) ? path[e] : 0.0;
+  }
+#pragma unroll
+  for (int rr = 0; rr < HB; ++rr) {
+    const double w = h.bfine[R0 + rr];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      acc[rr][i] = w * c0[i];
+      cb[rr][i] = 0.0;
+    }
+  }
+  for (int j = 1; j <= J; ++j) {
+    double v[EPT];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = e0 + threadIdx.x + i * NT;
+      v[i] = (e < h.MM) ? path[(size_t)j * MM + e] : 0.0;
+    }
+#pragma unroll
+    for (int rr = 0; rr < HB; ++rr) {
+      const double w = h.afine[R0 + 1 + rr - j];
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) acc[rr][i] = fma(w, v[i], acc[rr][i]);
+    }
+  }
+  // coarse bracket rows r = R0+1 .. R0+HB: -m^-a sum_{j<n} b_{j+r/m} (U_{n-j} - U_{n-j-1})
+  for (int j = 0; j < n; ++j) {
+    double inc[EPT];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = e0 + threadIdx.x + i * NT;
+      inc[i] = (e < h.MM) ? h.U[(size_t)(n - j) * MM + e] - h.U[(size_t)(n - j - 1) * MM + e] : 0.0;
+    }
+#pragma unroll
+    for (int rr = 0; rr < HB; ++rr) {
+      const double w = h.bfrac[(size_t)j * h.m + R0 + 1 + rr];
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) cb[rr][i] = fma(w, inc[i], cb[rr][i]);
+    }
+  }
+  double* out = h.far + (size_t)b * 2 * HB * MM;
+#pragma unroll
+  for (int rr = 0; rr < HB; ++rr)
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = e0 + threadIdx.x + i * NT;
+      if (e < h.MM) {
+        out[(size_t)rr * MM + e] = acc[rr][i];
+        out[(size_t)(HB + rr) * MM + e] = (n > 0) ? -h.minv * cb[rr][i] : 0.0;
+      }
+    }
+}
+
+// per substep r: HIST = far[rr] + near rows, CON = bracket[rr], X0 = extrapolation
+__global__ void k2_prep(Hist2DArgs h, int r, double* HIST, double* CON, double* X0) {
+  const int b = blockIdx.y;
+  const size_t MM = h.MM;
+  const int rr = (r - 1) % HB, beta = (r - 1) / HB;
+  const int J = (beta > 0 ? beta - 1 : 0) * HB;
+  const int p = r - 1 < EXO ? r - 1 : EXO;
+  const double* path = h.paths + (size_t)b * (h.m + 1) * MM;
+  const double* far = h.far + (size_t)b * 2 * HB * MM;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < MM; e += (size_t)gridDim.x * blockDim.x) {
+    double acc = far[(size_t)rr * MM + e];
+    for (int j = J + 1; j < r; ++j) acc = fma(h.afine[r - j], path[(size_t)j * MM + e], acc);
+    HIST[(size_t)b * MM + e] = acc;
+    CON[(size_t)b * MM + e] = far[(size_t)(HB + rr) * MM + e];
+    const double* w = kExtrap[p];
+    double g = w[0] * path[(size_t)(r - 1) * MM + e];
+    for (int j = 1; j <= p; ++j) g = fma(w[j], path[(size_t)(r - 1 - j) * MM + e], g);
+    X0[(size_t)b * MM + e] = g;
+  }
+}
+
+// coarse history of a coarse step: HIST = b_n U_0 + sum_{j=1}^{n} (b_{n-j} - b_{n-j+1}) U_j
+__global__ void k2_coarse_hist(const double* H, int n, long MM, const double* bfine, double* HIST) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < (size_t)MM; e += (size_t)gridDim.x * blockDim.x) {
+    double acc = bfine[n] * H[e];
+    for (int j = 1; j <= n; ++j) acc = fma(bfine[n - j] - bfine[n - j + 1], H[(size_t)j * MM + e], acc);
+    HIST[e] = acc;
+  }
+}
+
+// U_next[n+1] = F_old[n] + (G_new[n] - G_old[n])
+__global__ void k2_correct_row(const double* fold, const double* gnew, const double* gold, double* unext, long MM) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < (size_t)MM; e += (size_t)gridDim.x * blockDim.x)
+    unext[e] = fold[e] + (gnew[e] - gold[e]);
+}
+
+// node norms / diff for the guards (parareal.py:120-128): one CTA per node, fixed order
+__global__ void k2_node_norms(const double* unext, const double* ucur, long MM, double* out /* (nt+1, 3) */) {
+  const int n = blockIdx.x;
+  __shared__ double red[2 * 256];
+  double s0 = 0.0, s1 = 0.0;
+  int fin = 1;
+  for (size_t e = threadIdx.x; e < (size_t)MM; e += blockDim.x) {
+    const double v = unext[(size_t)n * MM + e];
+    const double d = v - ucur[(size_t)n * MM + e];
+    if (!isfinite(v)) fin = 0;
+    s0 = fma(v, v, s0);
+    s1 = fma(d, d, s1);
+  }
+  red[2 * threadIdx.x] = s0;
+  red[2 * threadIdx.x + 1] = s1;
+  const int allfin = __syncthreads_and(fin);
+  if (threadIdx.x == 0) {
+    double a = 0.0, c = 0.0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      a += red[2 * i];
+      c += red[2 * i + 1];
+    }
+    out[3 * n] = sqrt(a);
+    out[3 * n + 1] = sqrt(c);
+    out[3 * n + 2] = allfin ? 1.0 : 0.0;
+  }
+}
+
+}  // namespace pf
