@@ -126,7 +126,22 @@ def sweep_flops(M, m, slices, n_lo, pcg_iterations, solves):
     return f
 
 
-def history_bytes(M, m, slices, hb=16):
+def sweep_flops_2d(M, m, slices, n_lo, pcg_iterations):
+    """2-D sweep work per launch: setup = 4M + 4Q line FFTs, each PCG iteration
+    2M + 2Q line FFTs (length Q, 5 Q log2 Q), history 2 (r+1) M^2, bracket 2 n M^2,
+    pointwise 40 Q^2 per setup and 6 Q^2 per iteration."""
+    Q = 2 * M
+    fft = 5.0 * Q * math.log2(Q)
+    units = slices * m
+    it = pcg_iterations
+    f = units * (4 * M + 4 * Q) * fft + it * (2 * M + 2 * Q) * fft
+    f += slices * (m * (m + 1) + m) * M * M
+    f += sum(2.0 * n * M * M * m for n in range(n_lo, n_lo + slices))
+    f += 40.0 * Q * Q * units + 6.0 * Q * Q * it
+    return f
+
+
+def history_bytes(M, m, slices, hb=8):
     """HBM bytes of the blocked history: each path row read once per block + written once."""
     rows_read = sum(((r0 + 1)) for r0 in range(0, m, hb))
     return slices * 8.0 * M * (rows_read + (m + 1) + m * (hb // 2) / hb)
@@ -143,22 +158,27 @@ def cpu_sample(cfg_id, nt, target_s=15.0, lo=0, hi=None):
     M, m = cfg["modes"], cfg["m"]
     hi = nt if hi is None else hi
     prob = config_problem(cfg_id)
-    space = oracle.Sine1D(M)
+    dims = cfg["dims"]
+    space = oracle.Sine1D(M) if dims == 1 else oracle.Sine2D(M, pcg_tol=cfg.get("pcg_tol", 1e-13))
     grids = oracle.TimeGrids(cfg["t_final"], nt, m)
-    # coarse states: a few oracle coarse steps are cheap; the sample only needs
-    # realistic inputs, so use the initial coarse trajectory
-    U = oracle.run_coarse(prob, space, grids)
+    # the sample's timing does not depend on the coarse states: every slice
+    # starts from the initial state (no coarse sweep on the CPU)
+    u0 = space.initial_state(prob)
+    U = np.tile(u0, (nt + 1, 1))
+    if dims == 2:
+        hi = min(hi, lo + 4)  # 2-D oracle solves cost seconds each: sample 4 slices
     t0 = time.perf_counter()
-    oracle.fine_sweep_intervals(U, lo, hi, space, grids, prob, substeps=2)
-    per = (time.perf_counter() - t0) / 2.0
-    sub = max(2, min(m, int(target_s / max(per, 1e-9))))
+    oracle.fine_sweep_intervals(U, lo, hi, space, grids, prob, substeps=1)
+    per = time.perf_counter() - t0
+    sub = max(1, min(m, int(target_s / max(per, 1e-9))))
     t0 = time.perf_counter()
     oracle.fine_sweep_intervals(U, lo, hi, space, grids, prob, substeps=sub)
     dt = time.perf_counter() - t0
     units = (hi - lo) * sub
-    return {"value": units * M / dt, "unit": "mode-steps/s", "cores": os.cpu_count(), "kind": "port",
+    how = ("dense numpy assembly + batched LU" if dims == 1 else "matrix-free numpy PCG, dense transforms")
+    return {"value": units * M ** dims / dt, "unit": "mode-steps/s", "cores": os.cpu_count(), "kind": "port",
             "sample": f"{hi - lo} slices x {sub} of {m} substeps of config {cfg_id} "
-                      f"(oracle sine-Galerkin port: dense numpy assembly + batched LU, OpenBLAS threads)",
+                      f"(oracle sine-Galerkin port: {how}, OpenBLAS threads)",
             "seconds": dt}
 
 
@@ -175,7 +195,7 @@ def run_reference_arm(args, rank, world):
                                lo=0, hi=cfg["nt"]))
     vals = vals[args.warmup:]
     v = statistics.median(x["value"] for x in vals)
-    ms = 1e3 * cfg["nt"] * cfg["m"] * cfg["modes"] / v
+    ms = 1e3 * cfg["nt"] * cfg["m"] * cfg["modes"] ** cfg["dims"] / v
     line = {
         "impl": "reference", "metric": "fine mode-steps/s", "value": v, "unit": "mode-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -188,14 +208,16 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def _config_dict(cfg_id, world):
+def _config_dict(cfg_id, world, per_gpu=None):
     from paper_2510_11023_b200.problems import CONFIGS
 
-    cfg = CONFIGS[cfg_id]
-    return {"workload": f"config{cfg_id}: 1-D sine Galerkin fine sweep", "modes": cfg["modes"],
+    cfg = dict(CONFIGS[cfg_id])
+    if per_gpu is not None:
+        cfg["nt"] = per_gpu
+    return {"workload": f"config{cfg_id}: {cfg['dims']}-D sine Galerkin fine sweep", "modes": cfg["modes"],
             "slices_per_gpu": cfg["nt"], "slices_total": cfg["nt"] * world, "fine_steps_per_slice": cfg["m"],
             "alpha": cfg["alpha"], "t_final": cfg["t_final"], "parallelism": f"slices sharded over {world} GPU(s)",
-            "l2": "inputs larger than L2 (history paths > 126 MB)" if cfg_id == 3 else "inputs fit in L2"}
+            "l2": "inputs larger than L2 (history paths > 126 MB)" if cfg_id >= 3 else "inputs fit in L2"}
 
 
 # --------------------------------------------------------------------------
@@ -206,7 +228,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=3, choices=(1, 2, 3))
+    ap.add_argument("--config", type=int, default=3, choices=(1, 2, 3, 4, 5))
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -234,9 +256,12 @@ def main():
 
     cfg = CONFIGS[args.config]
     M, m, P_rank = cfg["modes"], cfg["m"], cfg["nt"]
+    dims = cfg["dims"]
+    if args.config == 5 and world == 1:
+        P_rank = 64  # config 5 is the scaling run: 64 slices per GPU (BASELINE.json)
     P = P_rank * world
     prob = pfb.config_problem(args.config)
-    op = pfb.build_sine_operator(M)
+    op = pfb.build_sine_operator(M, dims=dims)
     grids = pfb.TimeGrids(cfg["t_final"], P, m)
     lo, hi = block_bounds(P, world)[rank]
     ctx = _lib.context_for(prob, op, grids, device=local)
@@ -245,9 +270,11 @@ def main():
     torch.cuda.set_stream(stream)
     _lib.lib.pf_set_stream(ctx.handle, _lib.C.c_void_p(stream.cuda_stream))
 
-    traj = pfb.run_coarse(prob, op, grids)  # untimed: inputs of the sweep
+    # untimed inputs of the sweep: the coarse trajectory (1-D); the 2-D coarse
+    # sweep is P sequential PCG solves, so 2-D slices start from the initial state
+    traj = pfb.run_coarse(prob, op, grids) if dims == 1 else np.tile(pfb.initial_state(prob, op), (P + 1, 1))
     U = torch.from_numpy(traj).to(f"cuda:{local}")
-    out = torch.empty((hi - lo, M), dtype=torch.float64, device=f"cuda:{local}")
+    out = torch.empty((hi - lo, M ** dims), dtype=torch.float64, device=f"cuda:{local}")
 
     def step():
         ctx.check(_lib.lib.pf_dev_fine_sweep_async(ctx.handle, _lib.C.c_void_p(U.data_ptr()), lo, hi,
@@ -262,7 +289,7 @@ def main():
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    launches0 = ctx.stats()["fine_launches"]
+    launches0 = ctx.stats()["kernel_launches"]
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
@@ -271,7 +298,7 @@ def main():
         torch.cuda.synchronize()
     ctx.check(_lib.lib.pf_dev_check(ctx.handle))  # decodes the last launch's status (+ its counters)
     st = ctx.stats()
-    launches = st["fine_launches"] - launches0
+    launches = st["kernel_launches"] - launches0
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
@@ -279,10 +306,11 @@ def main():
         ms = float(t.item())
         dist.barrier()
     units_total = P * m
-    value = units_total * M / (ms / 1e3)
+    value = units_total * M ** dims / (ms / 1e3)
 
     # roofline of the dominant (only) kernel in the step
-    flops = sweep_flops(M, m, hi - lo, lo, st["pcg_iterations"], st["solves"])
+    flops = (sweep_flops(M, m, hi - lo, lo, st["pcg_iterations"], st["solves"]) if dims == 1
+             else sweep_flops_2d(M, m, hi - lo, lo, st["pcg_iterations"]))
     achieved_tf = flops / (ms / 1e3) / 1e12
     peaks = _peaks()
     roof = {"bound": "tensor", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -291,8 +319,8 @@ def main():
                            "MEASURED_PEAKS.json has HBM and bf16 only",
             "flops_per_launch": flops, "pcg_iterations_per_launch": st["pcg_iterations"],
             "pcg_iterations_per_solve": st["pcg_iterations"] / max(st["solves"], 1),
-            "hbm_bytes_per_launch": history_bytes(M, m, hi - lo),
-            "hbm_frac": history_bytes(M, m, hi - lo) / (ms / 1e3) / 1e9 / peaks.get("hbm_gbs", 6537.0)}
+            "hbm_bytes_per_launch": history_bytes(M ** dims, m, hi - lo),
+            "hbm_frac": history_bytes(M ** dims, m, hi - lo) / (ms / 1e3) / 1e9 / peaks.get("hbm_gbs", 6537.0)}
     try:
         with open(os.path.join(ROOT, "profiles", f"dram_config{args.config}.json")) as f:
             roof["traffic"] = json.load(f).get("dram_bytes_per_launch")
@@ -313,12 +341,12 @@ def main():
         t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": units_total * M / e2e_s, "unit": "mode-steps/s",
-           "h2d_bytes_per_step": int(hi * M * 8), "d2h_bytes_per_step": int((hi - lo) * M * 8),
+    e2e = {"value": units_total * M ** dims / e2e_s, "unit": "mode-steps/s",
+           "h2d_bytes_per_step": int(hi * M ** dims * 8), "d2h_bytes_per_step": int((hi - lo) * M ** dims * 8),
            "api": "paper_2510_11023_b200.fine_sweep_intervals (ctypes -> pf_fine_sweep)"}
 
     parareal = None
-    if not args.no_parareal and world == 1:
+    if not args.no_parareal and world == 1 and dims == 1:
         t0 = time.perf_counter()
         it, rep = pfb.parareal_solve(prob, op, grids, tol=cfg["tol"], k_max=P + 1)
         parareal = {"time_to_tol_s": time.perf_counter() - t0, "iterations": rep.iterations,
@@ -336,7 +364,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE config RNG convention, SURVEY.md §8d)",
-            "config": _config_dict(args.config, world), "roofline": roof, "cpu_baseline": cpu,
+            "config": _config_dict(args.config, world, P_rank), "roofline": roof, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "parareal": parareal,
         }
         print(json.dumps(line), flush=True)

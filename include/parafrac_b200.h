@@ -117,6 +117,7 @@ typedef struct {
   double last_fine_ms;          /* device time of the last fine-sweep launch    */
   double last_coarse_ms;        /* device time of the last coarse-kernel launch */
   long long helper_launches;    /* fine sweeps that ran with far-history helper CTAs */
+  long long kernel_launches;    /* every kernel this context launched */
 } pf_stats;
 
 /* ---- lifecycle ---------------------------------------------------------- */

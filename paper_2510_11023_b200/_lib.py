@@ -58,7 +58,7 @@ class pf_stats(C.Structure):
     _fields_ = [("fine_launches", C.c_longlong), ("coarse_launches", C.c_longlong),
                 ("pcg_iterations", C.c_longlong), ("solves", C.c_longlong),
                 ("last_fine_ms", C.c_double), ("last_coarse_ms", C.c_double),
-                ("helper_launches", C.c_longlong)]
+                ("helper_launches", C.c_longlong), ("kernel_launches", C.c_longlong)]
 
 
 # name -> (restype, argtypes); every symbol include/parafrac_b200.h declares

@@ -256,6 +256,7 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   PF_CUDA(c, cudaGetLastError());
   PF_CUDA(c, cudaEventRecord(c->ev1, c->stream));
   c->stats.fine_launches += 1;
+  c->stats.kernel_launches += 1;
   return 0;
 }
 
@@ -268,6 +269,7 @@ int launch_coarse(pf_ctx* c, const pf::CoarseArgs& a, Status* d_st) {
   });
   PF_CUDA(c, cudaGetLastError());
   c->stats.coarse_launches += 1;
+  c->stats.kernel_launches += 1;
   return 0;
 }
 
