@@ -208,27 +208,31 @@ int ensure_status(pf_ctx* c, int n) {
 // Launch the fine sweep for slices [n_lo, n_lo+bs) reading device states d_u.
 // When 2*bs CTAs fit on the device at once, launch cooperatively with one
 // helper CTA per slice (far history on otherwise idle SMs); else inline.
-int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, Status* d_st) {
+int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, Status* d_st, int m_override = 0,
+                int hps_req = 1) {
   if (c->kind == PF_SPACE_SINE2D) return e2_fine_sweep(c, d_u, n_lo, bs, d_out, c->grid.m, true);
-  if (c->paths.ensure((size_t)bs * (c->grid.m + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "paths");
-  if (c->scratch.ensure((size_t)bs * 4 * pf::HB * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
-  if (c->sync_cap < bs) {
+  const int m = m_override > 0 ? m_override : c->grid.m;
+  const int hps = std::max(1, hps_req);
+  if (c->paths.ensure((size_t)bs * (m + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "paths");
+  if (c->scratch.ensure((size_t)bs * 2 * (hps + 1) * 2 * pf::HB * c->size))
+    return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
+  const int nsync = bs * (2 + hps);
+  if (c->sync_cap < nsync) {
     if (c->d_sync) cudaFree(c->d_sync);
     c->d_sync = nullptr;
     c->sync_cap = 0;
-    PF_CUDA(c, cudaMalloc(&c->d_sync, sizeof(int) * 3 * bs));
-    c->sync_cap = bs;
+    PF_CUDA(c, cudaMalloc(&c->d_sync, sizeof(int) * nsync));
+    c->sync_cap = nsync;
   }
-  pf::SweepSync sync{c->d_sync, c->d_sync + bs, c->d_sync + 2 * bs};
-  PF_CUDA(c, cudaMemsetAsync(c->d_sync, 0, sizeof(int) * 3 * bs, c->stream));
+  pf::SweepSync sync{c->d_sync, c->d_sync + bs, c->d_sync + bs + bs * hps};
+  PF_CUDA(c, cudaMemsetAsync(c->d_sync, 0, sizeof(int) * nsync, c->stream));
   pf::Common cm = make_common(c);
+  cm.m = m;
   double* dp = c->paths.p;
   PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
   PF_DISPATCH(c, {
     auto kern = pf::k_fine_sweep<SP, SPP, NT, EPT>;
-    PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
     int per_sm = 0;
-    PF_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, c->smem));
     // shared-memory ring of the last NR states behind the space's own smem
     const size_t ring_bytes = sizeof(double) * pf::NR * c->size;
     const size_t base = (c->smem + 15) & ~size_t(15);
@@ -240,18 +244,19 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
     }
     PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     PF_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-    int helpers = (c->allow_helpers && 2 * bs <= per_sm * c->num_sms) ? 1 : 0;
+    int helpers = (c->allow_helpers && bs * (1 + hps) <= per_sm * c->num_sms) ? hps : 0;
+    if (!helpers && hps > 1) return set_error(c, PF_ERR_UNSUPPORTED, "split-K helpers do not fit on the device");
     int nsl = bs;
+    int smem_total = (int)smem;
     if (helpers) {
-      int smem_total = (int)smem;
       void* args[] = {(void*)&cm, (void*)&spp, (void*)&d_u, (void*)&n_lo, (void*)&nsl, (void*)&helpers,
                       (void*)&ring_off, (void*)&smem_total, (void*)&sync, (void*)&dp, (void*)&d_out, (void*)&d_st};
-      PF_CUDA(c, cudaLaunchCooperativeKernel((void*)kern, dim3(2 * bs), dim3(NT), args, smem, c->stream));
+      PF_CUDA(c, cudaLaunchCooperativeKernel((void*)kern, dim3(bs * (1 + hps)), dim3(NT), args, smem, c->stream));
     } else {
-      kern<<<bs, NT, smem, c->stream>>>(cm, spp, d_u, n_lo, nsl, 0, ring_off, (int)smem, sync, dp, d_out, d_st);
+      kern<<<bs, NT, smem, c->stream>>>(cm, spp, d_u, n_lo, nsl, 0, ring_off, smem_total, sync, dp, d_out, d_st);
     }
     c->last_helpers = helpers;
-    c->stats.helper_launches += helpers;
+    c->stats.helper_launches += helpers ? 1 : 0;
   });
   PF_CUDA(c, cudaGetLastError());
   PF_CUDA(c, cudaEventRecord(c->ev1, c->stream));
@@ -749,19 +754,24 @@ int pf_fine_sequential(pf_ctx* c, const double* u0, double* states) {
     PF_CUDA(c, cudaStreamSynchronize(c->stream));
     return 0;
   }
-  if (c->paths.ensure((size_t)(total + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "hist");
-  if (upload(c, c->paths.p, u0, c->size)) return c->err.code;
-  pf::Common cm = make_common(c);
-  double* dh = c->paths.p;
-  PF_DISPATCH(c, {
-    auto kern = pf::k_sequential<SP, SPP, NT, EPT>;
-    PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
-    kern<<<1, NT, c->smem, c->stream>>>(cm, spp, dh, (int)total, c->d_status);
-  });
-  PF_CUDA(c, cudaGetLastError());
+  // stepping.run_fine_sequential is slice 0 marched over nt*m fine substeps with the
+  // full history (no bracket since n = 0, t = (jj-1) dt): the sweep kernel with
+  // m = nt*m and the far history split over up to SMs-1 helper CTAs.
+  if (c->io.ensure((size_t)2 * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "io");
+  if (upload(c, c->io.p, u0, c->size)) return c->err.code;
+  if (ensure_status(c, 1)) return c->err.code;
+  const int hps = (int)std::max<long>(1, std::min<long>(c->num_sms - 1, total / 1024));
+  int rc = launch_fine(c, c->io.p, 0, 1, c->io.p + c->size, c->d_status, (int)total, hps);
+  if (rc == PF_ERR_UNSUPPORTED) rc = launch_fine(c, c->io.p, 0, 1, c->io.p + c->size, c->d_status, (int)total, 1);
+  if (rc) return rc;
   for (int n = 0; n <= c->grid.nt; ++n)
-    if (download(c, states + (size_t)n * c->size, dh + (size_t)n * c->grid.m * c->size, c->size)) return c->err.code;
-  int rc = decode_coarse(c, 0, 0);
+    if (download(c, states + (size_t)n * c->size, c->paths.p + (size_t)n * c->grid.m * c->size, c->size))
+      return c->err.code;
+  rc = decode_fine(c, 0, 1);
+  if (rc == PF_ERR_SOLVER || rc == PF_ERR_COEFFICIENT) {  // SolverFailure(jj - 1), stepping.py:286
+    c->err.step_n = c->err.step_r - 1;
+    c->err.step_r = -1;
+  }
   return rc;
 }
 

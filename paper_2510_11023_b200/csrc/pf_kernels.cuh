@@ -5,7 +5,8 @@
 //   k_coarse       one CTA; run_coarse / the parareal correction sweep with
 //                  guards and diff / a single coarse step
 //                  (stepping.py:87-121, parareal.py:114-128)
-//   k_sequential   one CTA; the full-history fine solver (stepping.py:260-288)
+//   (the full-history solver, stepping.py:260-288, is k_fine_sweep over one
+//   slice of nt*m substeps with split-K helper CTAs)
 //
 // Thread ownership of state entries is e = threadIdx.x + i*NT (i < EPT) in
 // every kernel, so a thread only ever re-reads history rows it wrote itself.
@@ -151,48 +152,6 @@ __device__ __forceinline__ void bracket_block(const Common& c, const double* __r
     }
 }
 
-// L1 history of one slice at substep r (einsum at stepping.py:234):
-//   h = b_{r-1} path[0] + sum_{j=1}^{r-1} (b_{r-j-1} - b_{r-j}) path[j]
-template <int NT, int EPT>
-__device__ __forceinline__ void history_sum(const Common& c, const double* path, int r,
-                                            double* h) {
-  const double* __restrict__ b = c.bfine;
-  const double b0 = b[r - 1];
-#pragma unroll
-  for (int i = 0; i < EPT; ++i) {
-    const int e = threadIdx.x + i * NT;
-    h[i] = (e < c.size) ? b0 * path[e] : 0.0;
-  }
-  int j = 1;
-  for (; j + 3 < r; j += 4) {
-    const double w0 = b[r - j - 1] - b[r - j];
-    const double w1 = b[r - j - 2] - b[r - j - 1];
-    const double w2 = b[r - j - 3] - b[r - j - 2];
-    const double w3 = b[r - j - 4] - b[r - j - 3];
-    const double* p0 = path + (size_t)j * c.size;
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int e = threadIdx.x + i * NT;
-      if (e < c.size) {
-        const double v0 = p0[e], v1 = p0[c.size + e], v2 = p0[2 * c.size + e], v3 = p0[3 * c.size + e];
-        double acc = fma(w0, v0, h[i]);
-        acc = fma(w1, v1, acc);
-        acc = fma(w2, v2, acc);
-        h[i] = fma(w3, v3, acc);
-      }
-    }
-  }
-  for (; j < r; ++j) {
-    const double w = b[r - j - 1] - b[r - j];
-    const double* p0 = path + (size_t)j * c.size;
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int e = threadIdx.x + i * NT;
-      if (e < c.size) h[i] = fma(w, p0[e], h[i]);
-    }
-  }
-}
-
 // coarse-history bracket of slice n for target (n, r)  (stepping.py:124-139):
 //   -m^-alpha sum_{j=0}^{n-1} b_{j + r/m} (U_{n-j} - U_{n-j-1})
 template <int NT, int EPT>
@@ -268,10 +227,17 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   extern __shared__ __align__(16) char smem[];
   constexpr int JT = (EPT > 2 ? 4 : 8);  // rows per register chunk (x2 double-buffered)
   const bool helper = (int)blockIdx.x >= nslices;
-  const int b = helper ? (int)blockIdx.x - nslices : (int)blockIdx.x;
+  // `helpers` = helper CTAs per slice (0: far history inline).  With K > 1 the
+  // far-history rows are split by row blocks (block rb -> helper rb mod K) and
+  // the slice CTA sums the K partial tiles in fixed order (split-K).
+  const int hps = helpers > 0 ? helpers : 1;
+  const int b = helper ? ((int)blockIdx.x - nslices) / hps : (int)blockIdx.x;
+  const int hid = helper ? ((int)blockIdx.x - nslices) % hps : 0;
   const int n = n_lo + b;
   double* path = paths + (size_t)b * (c.m + 1) * c.size;
-  double* scr = c.scratch + (size_t)b * 4 * HB * c.size;  // [parity][hist|bracket][HB][size]
+  // per slice: [parity][hps + 1][hist | bracket][HB][size]; tile hps is the combined one
+  double* scr = c.scratch + (size_t)b * 2 * (hps + 1) * 2 * HB * c.size;
+  auto slot = [&](int parity, int h) { return scr + ((size_t)parity * (hps + 1) + h) * 2 * HB * c.size; };
   const int nblocks = (c.m + HB - 1) / HB;
   if (helper) {
     // Toeplitz weights a_s into shared memory once (helpers own the SM's smem)
@@ -282,7 +248,6 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       __syncthreads();
       aw = s_aw;
     }
-    // path row 0 is the slice's start state, readable from U directly
     for (int beta = 0; beta < nblocks; ++beta) {
       const int J = far_extent(beta);
       if (J > 0) {
@@ -296,10 +261,34 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         __syncthreads();
         if (ld_acquire(sync.abort + b) != 0) return;
       }
-      double* hs = scr + (size_t)(beta & 1) * 2 * HB * c.size;
-      far_history_block<NT, EPT, JT>(c, J > 0 ? path : U + (size_t)n * c.size, aw, beta * HB, J, hs);
-      bracket_block<NT, EPT>(c, U, n, beta * HB + 1, hs + (size_t)HB * c.size);
-      cta_publish(sync.ready + b, beta + 1);
+      double* hs = slot(beta & 1, hid);
+      const int R0 = beta * HB;
+      // this helper's rows: blocks rb = hid, hid + hps, ... of HB rows starting at row 1
+      double acc[HB][EPT];
+      {
+        const double* row0 = J > 0 ? path : U + (size_t)n * c.size;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+          const int e = threadIdx.x + i * NT;
+          const double c0 = (hid == 0 && e < c.size) ? __ldcg(row0 + e) : 0.0;
+#pragma unroll
+          for (int rr = 0; rr < HB; ++rr) acc[rr][i] = c.bfine[R0 + rr] * c0;
+        }
+      }
+      for (int rb = hid; 1 + rb * HB <= J; rb += hps) {
+        double cv[HB][EPT];
+        load_rows<NT, EPT, HB>(c, path, 1 + rb * HB, J, cv);
+        fma_rows<EPT, HB>(aw, R0, 1 + rb * HB, cv, acc);
+      }
+#pragma unroll
+      for (int rr = 0; rr < HB; ++rr)
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+          const int e = threadIdx.x + i * NT;
+          if (e < c.size) hs[(size_t)rr * c.size + e] = acc[rr][i];
+        }
+      if (hid == 0) bracket_block<NT, EPT>(c, U, n, R0 + 1, hs + (size_t)HB * c.size);
+      cta_publish(sync.ready + b * hps + hid, beta + 1);
     }
     return;
   }
@@ -332,15 +321,40 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     PF_T(10);
     if (rr == 0) {
       J = far_extent(beta);
-      double* slot = scr + (size_t)(beta & 1) * 2 * HB * c.size;
+      double* s0 = slot(beta & 1, 0);
       if (helpers) {
         cta_publish(sync.progress + b, r - 1);  // rows 0..r-1 are in the path
-        cta_wait_geq(sync.ready + b, beta + 1);
+        if (threadIdx.x == 0) {
+          for (int h = 0; h < hps; ++h) {
+            int ns = 64;
+            while (ld_acquire(sync.ready + b * hps + h) < beta + 1) {
+              __nanosleep(ns);
+              ns = ns < 2048 ? 2 * ns : ns;
+            }
+          }
+        }
+        __syncthreads();
+        if (hps > 1) {  // combine the split-K partial tiles (fixed order) into tile hps
+          double* cmb = slot(beta & 1, hps);
+#pragma unroll
+          for (int i = 0; i < EPT; ++i) {
+            const int e = threadIdx.x + i * NT;
+            if (e < c.size) {
+              for (int q = 0; q < HB; ++q) {
+                double acc = 0.0;
+                for (int h = 0; h < hps; ++h) acc += __ldcg(slot(beta & 1, h) + (size_t)q * c.size + e);
+                cmb[(size_t)q * c.size + e] = acc;
+                cmb[(size_t)(HB + q) * c.size + e] = __ldcg(s0 + (size_t)(HB + q) * c.size + e);
+              }
+            }
+          }
+          s0 = cmb;
+        }
       } else {
-        far_history_block<NT, EPT, JT>(c, path, c.afine, beta * HB, J, slot);
-        bracket_block<NT, EPT>(c, U, n, r, slot + (size_t)HB * c.size);
+        far_history_block<NT, EPT, JT>(c, path, c.afine, beta * HB, J, s0);
+        bracket_block<NT, EPT>(c, U, n, r, s0 + (size_t)HB * c.size);
       }
-      hs = slot;
+      hs = s0;
 #pragma unroll
       for (int i = 0; i < EPT; ++i) {
         const int e = threadIdx.x + i * NT;
@@ -550,46 +564,6 @@ __global__ void __launch_bounds__(NT) k_coarse(Common c, SPP spp, CoarseArgs a, 
         st.r = 1;
       }
       if (threadIdx.x == 0) a.out[0] = dmax;
-    }
-  }
-  if (threadIdx.x == 0) status[0] = st;
-}
-
-// full-history fine solver (stepping.py:260-288); hist has (total+1) rows
-template <class SP, class SPP, int NT, int EPT>
-__global__ void __launch_bounds__(NT) k_sequential(Common c, SPP spp, double* hist, int total,
-                                                   Status* __restrict__ status) {
-  extern __shared__ __align__(16) char smem[];
-  SP sp;
-  sp.init(smem, spp);
-  Status st = {ST_OK, 0, -1, -1, 0, 0, {0, 0}};
-  double x[EPT], xpp[EPT];
-#pragma unroll
-  for (int i = 0; i < EPT; ++i) {
-    const int e = threadIdx.x + i * NT;
-    x[i] = (e < c.size) ? hist[e] : 0.0;
-    xpp[i] = x[i];
-  }
-  for (int jj = 1; jj <= total; ++jj) {
-    double h[EPT], z[EPT], xn[EPT];
-    history_sum<NT, EPT>(c, hist, jj, h);
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) z[i] = 0.0;
-    st.n = jj - 1;
-    double xg[EPT];
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) xg[i] = (jj > 1) ? fma(2.0, x[i], -xpp[i]) : x[i];
-    const int code = sp.step(c.fn, x, xg, (double)(jj - 1) * c.dt, c.gam_f, h, z, xn, st);
-    if (code != ST_OK) {
-      st.code = code;
-      break;
-    }
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int e = threadIdx.x + i * NT;
-      xpp[i] = x[i];
-      x[i] = xn[i];
-      if (e < c.size) hist[(size_t)jj * c.size + e] = x[i];
     }
   }
   if (threadIdx.x == 0) status[0] = st;
