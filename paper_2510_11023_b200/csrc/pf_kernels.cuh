@@ -192,12 +192,11 @@ __device__ __forceinline__ void cta_wait_geq(const int* flag, int v) {
   __syncthreads();
 }
 // the whole CTA's prior global writes become visible, then thread 0 publishes v
+// (bar.sync orders the CTA's writes before thread 0's st.release.gpu, and
+// release is cumulative in the PTX memory model: no separate membar.gl needed)
 __device__ __forceinline__ void cta_publish(int* flag, int v) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(flag, v);
-  }
+  if (threadIdx.x == 0) st_release(flag, v);
 }
 
 // History rows of block beta (target rows R0+1..R0+HB, R0 = beta*HB) folded
@@ -275,10 +274,17 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
           for (int rr = 0; rr < HB; ++rr) acc[rr][i] = c.bfine[R0 + rr] * c0;
         }
       }
-      for (int rb = hid; 1 + rb * HB <= J; rb += hps) {
-        double cv[HB][EPT];
-        load_rows<NT, EPT, HB>(c, path, 1 + rb * HB, J, cv);
-        fma_rows<EPT, HB>(aw, R0, 1 + rb * HB, cv, acc);
+      // owned row blocks, double-buffered: the next block's loads overlap this block's FMAs
+      if (1 + hid * HB <= J) {
+        double ca[HB][EPT], cb[HB][EPT];
+        load_rows<NT, EPT, HB>(c, path, 1 + hid * HB, J, ca);
+        for (int rb = hid; 1 + rb * HB <= J; rb += 2 * hps) {
+          load_rows<NT, EPT, HB>(c, path, 1 + (rb + hps) * HB, J, cb);
+          fma_rows<EPT, HB>(aw, R0, 1 + rb * HB, ca, acc);
+          if (1 + (rb + hps) * HB > J) break;
+          load_rows<NT, EPT, HB>(c, path, 1 + (rb + 2 * hps) * HB, J, ca);
+          fma_rows<EPT, HB>(aw, R0, 1 + (rb + hps) * HB, cb, acc);
+        }
       }
 #pragma unroll
       for (int rr = 0; rr < HB; ++rr)
@@ -385,18 +391,16 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       double acc = 0.0, cb = 0.0, g = x[i];
       if (e < c.size) {
         acc = hcur[i];
-        for (int j = J + 1; j < r; ++j) {
-          const double v = ring ? ring[(size_t)(j & (NR - 1)) * c.size + e] : path[(size_t)j * c.size + e];
-          acc = fma(s_anear[r - j], v, acc);
-        }
         cb = ccur[i];
         // extrapolated guess; row r-1 is x itself
         const double* w = kExtrap[p];
         g = w[0] * x[i];
-        for (int j = 1; j <= p; ++j) {
-          const int row = r - 1 - j;
-          const double v = ring ? ring[(size_t)(row & (NR - 1)) * c.size + e] : path[(size_t)row * c.size + e];
-          g = fma(w[j], v, g);
+        if (ring) {  // separate loops keep the ring loads in the shared address space
+          for (int j = J + 1; j < r; ++j) acc = fma(s_anear[r - j], ring[(j & (NR - 1)) * c.size + e], acc);
+          for (int j = 1; j <= p; ++j) g = fma(w[j], ring[((r - 1 - j) & (NR - 1)) * c.size + e], g);
+        } else {
+          for (int j = J + 1; j < r; ++j) acc = fma(s_anear[r - j], path[(size_t)j * c.size + e], acc);
+          for (int j = 1; j <= p; ++j) g = fma(w[j], path[(size_t)(r - 1 - j) * c.size + e], g);
         }
       }
       h[i] = acc;
