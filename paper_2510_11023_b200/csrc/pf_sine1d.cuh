@@ -260,7 +260,7 @@ struct Sine1D {
     PF_T(1);
     // --- pointwise coefficients (fused epilogue) ------------------------
     const double wq = 1.0 / (double)Q;
-    const double emt = exp(-t);
+    const double emt = fn.id == 1 ? exp(-t) : 0.0;  // only PF_FN_POLY's source uses exp(-t)
     double dsum = 0.0, nbad = 0.0;
     int bad = 0x7fffffff;
 #pragma unroll

@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(256) k2_cols(Sine2DArgs a) {
   const size_t gl = ((size_t)b * L::Q + q2) * L::Q;  // grid line base [b][q2][.]
   const double wq = 1.0 / ((double)L::Q * (double)L::Q);
   const double t = (double)(a.n0 + b) * a.dTs + a.tr;
-  const double emt = exp(-t);
+  const double emt = a.fn.id == 1 ? exp(-t) : 0.0;
   // grid values kept in registers between the synthesis and analysis FFTs
   constexpr int QPL = (L::Q + L::TPL - 1) / L::TPL;
   double gx[QPL], gy[QPL], uu[QPL];
@@ -676,18 +676,24 @@ __global__ void __launch_bounds__(NT) k2_far(Hist2DArgs h, int beta) {
       cb[rr][i] = 0.0;
     }
   }
-  for (int j = 1; j <= J; ++j) {
-    double v[EPT];
+  for (int j0 = 1; j0 <= J; j0 += 4) {  // 4 rows in flight per thread
+    double v[4][EPT];
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int e = e0 + threadIdx.x + i * NT;
-      v[i] = (e < h.MM) ? path[(size_t)j * MM + e] : 0.0;
-    }
+    for (int t = 0; t < 4; ++t)
 #pragma unroll
-    for (int rr = 0; rr < HB; ++rr) {
-      const double w = h.afine[R0 + 1 + rr - j];
+      for (int i = 0; i < EPT; ++i) {
+        const int e = e0 + threadIdx.x + i * NT;
+        v[t][i] = (e < h.MM && j0 + t <= J) ? path[(size_t)(j0 + t) * MM + e] : 0.0;
+      }
 #pragma unroll
-      for (int i = 0; i < EPT; ++i) acc[rr][i] = fma(w, v[i], acc[rr][i]);
+    for (int t = 0; t < 4; ++t) {
+      if (j0 + t > J) break;
+#pragma unroll
+      for (int rr = 0; rr < HB; ++rr) {
+        const double w = h.afine[R0 + 1 + rr - (j0 + t)];
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) acc[rr][i] = fma(w, v[t][i], acc[rr][i]);
+      }
     }
   }
   // coarse bracket rows r = R0+1 .. R0+HB: -m^-a sum_{j<n} b_{j+r/m} (U_{n-j} - U_{n-j-1})
