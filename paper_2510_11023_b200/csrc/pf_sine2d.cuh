@@ -97,6 +97,102 @@ __device__ __forceinline__ cd* fft_lines(cd* a, cd* b, const cd* __restrict__ tw
   return a;
 }
 
+// Twiddles of every radix-4 pass for this lane, kept in registers (the line
+// kernels are shared-memory-bandwidth bound; this removes 3 of the 11
+// shared-memory wavefronts per butterfly).  Valid when TPL == L/4.
+template <int LG>
+struct TwReg {
+  static constexpr int NP = LG / 2;  // radix-4 passes
+  cd w[NP > 0 ? NP : 1][3];
+  cd w2;  // final radix-2 pass (odd LG)
+  __device__ __forceinline__ void load(const cd* __restrict__ twp, int lane) {
+    int off = 0;
+#pragma unroll
+    for (int pass = 1; pass < NP; ++pass) {
+      const int Ns = 1 << (2 * pass);
+      const int k = lane & (Ns - 1);
+      w[pass][0] = twp[off + k];
+      w[pass][1] = twp[off + Ns + k];
+      w[pass][2] = twp[off + 2 * Ns + k];
+      off += 3 * Ns;
+    }
+    if (LG & 1) {
+      const int Ns = 1 << (LG - 1);
+      // radix-2 pass: L/2 butterflies, TPL = L/4 lanes -> two per lane (j = lane, lane + L/4)
+      w2 = twp[off + (lane & (Ns - 1))];
+    }
+  }
+};
+
+// Same arithmetic as fft_lines, with TwReg twiddles (TPL must equal L/4).
+template <int LG, bool INV>
+__device__ __forceinline__ cd* fft_lines_reg(cd* a, cd* b, const TwReg<LG>& tr, const cd* __restrict__ twp,
+                                             int lane) {
+  constexpr int L = 1 << LG;
+  constexpr int L4 = L >> 2;
+  int off = 0;
+#pragma unroll
+  for (int pass = 0; pass < LG / 2; ++pass) {
+    const int Ns = 1 << (2 * pass);
+    const int j = lane;
+    const int k = j & (Ns - 1);
+    cd v0 = a[sw(j)], v1 = a[sw(j + L4)], v2 = a[sw(j + 2 * L4)], v3 = a[sw(j + 3 * L4)];
+    if (pass > 0) {
+      cd w1 = tr.w[pass][0], w2 = tr.w[pass][1], w3 = tr.w[pass][2];
+      if (INV) {
+        w1.y = -w1.y;
+        w2.y = -w2.y;
+        w3.y = -w3.y;
+      }
+      v1 = cmul(v1, w1);
+      v2 = cmul(v2, w2);
+      v3 = cmul(v3, w3);
+    }
+    const cd t0 = cadd(v0, v2), t1 = csub(v0, v2), t2 = cadd(v1, v3), t3 = csub(v1, v3);
+    const cd mi3 = {t3.y, -t3.x};
+    const int base = ((j - k) << 2) + k;
+    b[sw(base)] = cadd(t0, t2);
+    b[sw(base + Ns)] = INV ? csub(t1, mi3) : cadd(t1, mi3);
+    b[sw(base + 2 * Ns)] = csub(t0, t2);
+    b[sw(base + 3 * Ns)] = INV ? cadd(t1, mi3) : csub(t1, mi3);
+    if (pass > 0) off += 3 * Ns;
+    __syncthreads();
+    cd* t = a;
+    a = b;
+    b = t;
+  }
+  if (LG & 1) {
+    constexpr int L2 = L >> 1;
+    constexpr int Ns = 1 << (LG - 1);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = lane + h * L4;
+      const int k = j & (Ns - 1);
+      cd v0 = a[sw(j)], v1 = a[sw(j + L2)];
+      cd w = (h == 0) ? tr.w2 : twp[off + k];
+      if (INV) w.y = -w.y;
+      v1 = cmul(v1, w);
+      const int base = ((j - k) << 1) + k;
+      b[sw(base)] = cadd(v0, v1);
+      b[sw(base + Ns)] = csub(v0, v1);
+    }
+    __syncthreads();
+    cd* t = a;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// line FFT dispatch: register twiddles when every lane owns one butterfly per pass
+template <int LG, int TPL, bool INV>
+__device__ __forceinline__ cd* line_fft(cd* a, cd* b, const TwReg<LG>& tr, const cd* __restrict__ twp, int lane) {
+  if constexpr (TPL == (1 << LG) / 4 && LG >= 2)
+    return fft_lines_reg<LG, INV>(a, b, tr, twp, lane);
+  else
+    return fft_lines<LG, TPL, INV>(a, b, twp, lane);
+}
+
 struct Sine2DArgs {
   Fn fn;
   int M, Q, B;              // modes per axis, grid per axis, systems in the batch
@@ -193,6 +289,8 @@ __global__ void __launch_bounds__(256) k2_rows_syn(Sine2DArgs a) {
   double* stage;
   line_setup<LG>(smem, a, twp, ph, A, B, stage);
   const int line = threadIdx.x / L::TPL, lane = threadIdx.x % L::TPL;
+  TwReg<LG> tr;
+  tr.load(twp, lane);
   const int k1 = blockIdx.x * L::TL + line + 1;  // x mode of this line
   const bool live = line < L::TL && k1 <= L::M;
   cd* W = A + line * L::Q;
@@ -224,7 +322,7 @@ __global__ void __launch_bounds__(256) k2_rows_syn(Sine2DArgs a) {
       }
     }
     __syncthreads();
-    cd* Rl = fft_lines<LG, L::TPL, true>(A + line * L::Q, B + line * L::Q, twp, lane);
+    cd* Rl = line_fft<LG, L::TPL, true>(A + line * L::Q, B + line * L::Q, tr, twp, lane);
     // stage s (sin) and c (cos) per line, then write [q2][k1] tiles
     double* s_sin = stage;  // TL * (Q+1)  (reused for both outputs in two rounds)
     for (int out = 0; out < 2; ++out) {
@@ -269,6 +367,8 @@ __global__ void __launch_bounds__(256) k2_cols(Sine2DArgs a) {
   double* stage;
   line_setup<LG>(smem, a, twp, ph, A, B, stage);
   const int line = threadIdx.x / L::TPL, lane = threadIdx.x % L::TPL;
+  TwReg<LG> tr;
+  tr.load(twp, lane);
   const int q2 = blockIdx.x * L::TL + line;
   const bool live = line < L::TL && q2 < L::Q;
   const size_t hl = ((size_t)b * L::Q + q2) * L::M;  // H line base [b][q2][.]
@@ -302,7 +402,7 @@ __global__ void __launch_bounds__(256) k2_cols(Sine2DArgs a) {
       }
     }
     __syncthreads();
-    cd* Rl = fft_lines<LG, L::TPL, true>(A + line * L::Q, B + line * L::Q, twp, lane);
+    cd* Rl = line_fft<LG, L::TPL, true>(A + line * L::Q, B + line * L::Q, tr, twp, lane);
     if (live) {
 #pragma unroll
       for (int i = 0; i < QPL; ++i) {
@@ -367,7 +467,7 @@ __global__ void __launch_bounds__(256) k2_cols(Sine2DArgs a) {
       }
     }
     __syncthreads();
-    cd* Zl = fft_lines<LG, L::TPL, false>(A + line * L::Q, B + line * L::Q, twp, lane);
+    cd* Zl = line_fft<LG, L::TPL, false>(A + line * L::Q, B + line * L::Q, tr, twp, lane);
     if (live) {
       for (int k = lane + 1; k <= L::M; k += L::TPL) {
         const double2 X = anal_read(Zl, ph, L::Q, k);
@@ -417,6 +517,8 @@ __global__ void __launch_bounds__(256) k2_rows_ana(Sine2DArgs a) {
   double* stage;
   line_setup<LG>(smem, a, twp, ph, A, B, stage);
   const int line = threadIdx.x / L::TPL, lane = threadIdx.x % L::TPL;
+  TwReg<LG> tr;
+  tr.load(twp, lane);
   const int k1b = blockIdx.x * L::TL;
   const int k1 = k1b + line + 1;
   const bool live = line < L::TL && k1 <= L::M;
@@ -442,7 +544,7 @@ __global__ void __launch_bounds__(256) k2_rows_ana(Sine2DArgs a) {
       }
     }
     __syncthreads();
-    cd* Zl = fft_lines<LG, L::TPL, false>(A + line * L::Q, B + line * L::Q, twp, lane);
+    cd* Zl = line_fft<LG, L::TPL, false>(A + line * L::Q, B + line * L::Q, tr, twp, lane);
     if (live) {
 #pragma unroll
       for (int i = 0; i < MPL; ++i) {
