@@ -68,7 +68,7 @@ struct pf_ctx {
   size_t smem = 0;
   std::vector<double> h_bfine, h_bfrac, h_nodes, h_d1, h_qw;
   // device tables
-  double *d_bfine = nullptr, *d_afine = nullptr, *d_bfrac = nullptr, *d_nodes = nullptr, *d_d1 = nullptr, *d_qw = nullptr;
+  double *d_bfine = nullptr, *d_afine = nullptr, *d_bfrac = nullptr, *d_ext0 = nullptr, *d_nodes = nullptr, *d_d1 = nullptr, *d_qw = nullptr;
   cd *d_tw = nullptr, *d_ph = nullptr;  // d_tw: per-pass twiddle tables
   long len_fine = 0, len_frac = 0;
   // work buffers
@@ -139,6 +139,7 @@ pf::Common make_common(const pf_ctx* c) {
   cm.afine = c->d_afine;
   cm.bfrac = c->d_bfrac;
   cm.scratch = c->scratch.p;
+  cm.ext0 = c->d_ext0;
   for (int s = 0; s < 16; ++s) cm.anear[s] = (s >= 1 && s < (long)c->h_bfine.size()) ? c->h_bfine[s - 1] - c->h_bfine[s] : 0.0;
   return cm;
 }
@@ -498,6 +499,25 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
   PF_CUDA(c, cudaMalloc(&c->d_afine, sizeof(double) * h_afine.size()));
   PF_CUDA(c, cudaMemcpy(c->d_afine, h_afine.data(), sizeof(double) * h_afine.size(), cudaMemcpyHostToDevice));
   PF_CUDA(c, cudaMemcpy(c->d_bfrac, c->h_bfrac.data(), sizeof(double) * need_frac, cudaMemcpyHostToDevice));
+  if (c->kind == PF_SPACE_SINE1D && alpha < 1.0) {
+    // slice-0 guess weights: Lagrange extrapolation to tau(r) from tau(r-1..r-1-p), tau(k) = (k dt)^alpha
+    const long rows = (long)nt * m + 1;
+    std::vector<double> ext((size_t)rows * 8, 0.0);
+    for (long r = 2; r < rows; ++r) {
+      const int p = (int)std::min<long>(r - 1, pf::EXO);
+      long double tau[pf::EXO + 1];
+      for (int j = 0; j <= p; ++j) tau[j] = powl((long double)(r - 1 - j) * (long double)c->dt, (long double)alpha);
+      const long double tr = powl((long double)r * (long double)c->dt, (long double)alpha);
+      for (int j = 0; j <= p; ++j) {
+        long double w = 1.0L;
+        for (int q = 0; q <= p; ++q)
+          if (q != j) w *= (tr - tau[q]) / (tau[j] - tau[q]);
+        ext[(size_t)r * 8 + j] = (double)w;
+      }
+    }
+    PF_CUDA(c, cudaMalloc(&c->d_ext0, sizeof(double) * ext.size()));
+    PF_CUDA(c, cudaMemcpy(c->d_ext0, ext.data(), sizeof(double) * ext.size(), cudaMemcpyHostToDevice));
+  }
   if (c->kind == PF_SPACE_SINE1D || c->kind == PF_SPACE_SINE2D) {
     const int ntw = std::max(pf::tw_table_size(c->lgQ), 1);
     std::vector<cd> tw(ntw), ph(c->Q);
@@ -545,7 +565,7 @@ void pf_destroy(pf_ctx* c) {
   if (!c) return;
   if (c->device >= 0) cudaSetDevice(c->device);
   for (DevBuf* b : {&c->U, &c->Unext, &c->paths, &c->fold, &c->gold, &c->gnew, &c->io, &c->scalar, &c->scratch}) b->release();
-  for (void* p : {(void*)c->d_bfine, (void*)c->d_afine, (void*)c->d_bfrac, (void*)c->d_nodes, (void*)c->d_d1, (void*)c->d_qw,
+  for (void* p : {(void*)c->d_bfine, (void*)c->d_afine, (void*)c->d_bfrac, (void*)c->d_ext0, (void*)c->d_nodes, (void*)c->d_d1, (void*)c->d_qw,
                   (void*)c->d_tw, (void*)c->d_ph, (void*)c->d_status, (void*)c->d_sync})
     if (p) cudaFree(p);
   if (c->ev0) cudaEventDestroy(c->ev0);

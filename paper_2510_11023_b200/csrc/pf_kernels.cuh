@@ -25,6 +25,9 @@ struct Common {
   const double* bfrac;                // b_{q/m}
   double* scratch;                    // per-slice block history / bracket rows
   double anear[16];                   // a_s for s < 16 (near-history weights, uniform loads)
+  // slice-0 PCG guess: Lagrange extrapolation in tau = t^alpha (the t^alpha
+  // initial layer defeats polynomial extrapolation in t), 8 weights per r
+  const double* ext0;
 };
 
 // Block length of the blocked L1 history: each history row is read once per
@@ -320,6 +323,11 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   const double* hs = nullptr;
   int J = 0;
   double hnext[EPT], cnext[EPT];  // this block's far rows, prefetched one substep ahead
+  // slice-0 tau-extrapolation weights, prefetched one substep ahead (uniform loads)
+  const bool tau_guess = (n == 0 && c.ext0 != nullptr);
+  double wnext[EXO + 1];
+#pragma unroll
+  for (int j = 0; j <= EXO; ++j) wnext[j] = tau_guess && c.m >= 2 ? c.ext0[(size_t)2 * 8 + j] : 0.0;
   for (int r = 1; r <= c.m; ++r) {
     const double t = (double)n * c.dT + (double)(r - 1) * c.dt;
     const int rr = (r - 1) % HB;
@@ -384,6 +392,13 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       }
     }
     const int p = r - 1 < EXO ? r - 1 : EXO;
+    double wcur[EXO + 1];
+    const bool use_tau = tau_guess && r >= 2;
+#pragma unroll
+    for (int j = 0; j <= EXO; ++j) {
+      wcur[j] = use_tau ? wnext[j] : kExtrap[p][j];
+      if (use_tau && r + 1 <= c.m) wnext[j] = c.ext0[(size_t)(r + 1) * 8 + j];
+    }
     double h[EPT], ct[EPT], xg[EPT], xn[EPT];
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
@@ -393,11 +408,20 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         acc = hcur[i];
         cb = ccur[i];
         // extrapolated guess; row r-1 is x itself
-        const double* w = kExtrap[p];
+        const double* w = wcur;
         g = w[0] * x[i];
-        if (ring) {  // separate loops keep the ring loads in the shared address space
-          for (int j = J + 1; j < r; ++j) acc = fma(s_anear[r - j], ring[(j & (NR - 1)) * c.size + e], acc);
-          for (int j = 1; j <= p; ++j) g = fma(w[j], ring[((r - 1 - j) & (NR - 1)) * c.size + e], g);
+        if (ring) {
+          // all NR-1 recent rows first (independent shared loads), then the two FMA chains;
+          // v[q-1] is the row at distance q (row r-q)
+          double v[NR - 1];
+#pragma unroll
+          for (int q = 1; q < NR; ++q) v[q - 1] = (r - q >= 0) ? ring[((r - q) & (NR - 1)) * c.size + e] : 0.0;
+#pragma unroll
+          for (int q = 1; q < NR; ++q)
+            if (r - q > J) acc = fma(s_anear[q], v[q - 1], acc);
+#pragma unroll
+          for (int j = 1; j <= EXO; ++j)
+            if (j <= p) g = fma(w[j], v[j], g);
         } else {
           for (int j = J + 1; j < r; ++j) acc = fma(s_anear[r - j], path[(size_t)j * c.size + e], acc);
           for (int j = 1; j <= p; ++j) g = fma(w[j], path[(size_t)(r - 1 - j) * c.size + e], g);

@@ -239,6 +239,35 @@ struct Sine1D {
   }
 
   // One semi-implicit substep.  xprev: owned coefficients of c_prev.
+  // fused pointwise epilogue for functor FID (0: generic dispatch)
+  template <int FID>
+  __device__ __forceinline__ void pointwise(const Fn& fn, cd* R, double t, double emt, double& dsum, double& nbad,
+                                            int& bad) {
+    const double wq = 1.0 / (double)Q;
+#pragma unroll
+    for (int i = 0; i < QPT; ++i) {
+      const int q = threadIdx.x + i * NT;
+      if (Q % NT == 0 || q < Q) {
+        const int s = sw(perm(q));
+        const cd w = R[s];
+        const double s1 = 0.5 * w.x, s2 = 0.5 * w.y;
+        const double u = (q & 1) ? -s1 : s1;
+        Fn f1 = fn;
+        if (FID != 0) f1.id = FID;  // constant-folds the functor switch
+        const double Dv = fn_D(f1, xq[q], 0.0, t, u);
+        if (!isfinite(Dv)) {
+          bad = min(bad, q);
+          nbad += 1.0;
+        }
+        const double d = wq * Dv;
+        const double g = wq * fn_f(f1, xtab[q], emt, u);
+        dq[q] = d;
+        dsum += d;
+        R[s] = {(q & 1) ? -g : g, d * s2};
+      }
+    }
+  }
+
   // xguess: PCG initial guess (the caller extrapolates from the path; it
   // only changes the iteration count, not the solution beyond pcg_tol).
   __device__ int step(const Fn& fn, const double* xprev, const double* xguess, double t, double gam,
@@ -259,29 +288,17 @@ struct Sine1D {
     cd* O = (R == A) ? B : A;
     PF_T(1);
     // --- pointwise coefficients (fused epilogue) ------------------------
-    const double wq = 1.0 / (double)Q;
     const double emt = fn.id == 1 ? exp(-t) : 0.0;  // only PF_FN_POLY's source uses exp(-t)
     double dsum = 0.0, nbad = 0.0;
     int bad = 0x7fffffff;
-#pragma unroll
-    for (int i = 0; i < QPT; ++i) {
-      const int q = threadIdx.x + i * NT;
-      if (Q % NT == 0 || q < Q) {
-        const int s = sw(perm(q));
-        const cd w = R[s];
-        const double s1 = 0.5 * w.x, s2 = 0.5 * w.y;
-        const double u = (q & 1) ? -s1 : s1;
-        const double Dv = fn_D(fn, xq[q], 0.0, t, u);
-        if (!isfinite(Dv)) {
-          bad = min(bad, q);
-          nbad += 1.0;
-        }
-        const double d = wq * Dv;
-        const double g = wq * fn_f(fn, xtab[q], emt, u);
-        dq[q] = d;
-        dsum += d;
-        R[s] = {(q & 1) ? -g : g, d * s2};
-      }
+    // one switch outside the point loop: each functor's loop is straight-line
+    // code, so the compiler interleaves the QPT transcendental evaluations
+    switch (fn.id) {
+      case 1: pointwise<1>(fn, R, t, emt, dsum, nbad, bad); break;
+      case 2: pointwise<2>(fn, R, t, emt, dsum, nbad, bad); break;
+      case 3: pointwise<3>(fn, R, t, emt, dsum, nbad, bad); break;
+      case 4: pointwise<4>(fn, R, t, emt, dsum, nbad, bad); break;
+      default: pointwise<0>(fn, R, t, emt, dsum, nbad, bad); break;
     }
     const double2 s01 = red.sum2(dsum, nbad);
     if (s01.y > 0.0) {
