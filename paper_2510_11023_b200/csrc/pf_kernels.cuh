@@ -277,16 +277,18 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
           for (int rr = 0; rr < HB; ++rr) acc[rr][i] = c.bfine[R0 + rr] * c0;
         }
       }
-      // owned row blocks, double-buffered: the next block's loads overlap this block's FMAs
-      if (1 + hid * HB <= J) {
-        double ca[HB][EPT], cb[HB][EPT];
-        load_rows<NT, EPT, HB>(c, path, 1 + hid * HB, J, ca);
-        for (int rb = hid; 1 + rb * HB <= J; rb += 2 * hps) {
-          load_rows<NT, EPT, HB>(c, path, 1 + (rb + hps) * HB, J, cb);
-          fma_rows<EPT, HB>(aw, R0, 1 + rb * HB, ca, acc);
-          if (1 + (rb + hps) * HB > J) break;
-          load_rows<NT, EPT, HB>(c, path, 1 + (rb + 2 * hps) * HB, J, ca);
-          fma_rows<EPT, HB>(aw, R0, 1 + (rb + hps) * HB, cb, acc);
+      // owned row chunks of CH rows (chunk rb -> helper rb mod hps), double-buffered:
+      // the next chunk's loads overlap this chunk's FMAs (2*CH*EPT loads in flight)
+      constexpr int CH = EPT > 2 ? 8 : 16;
+      if (1 + hid * CH <= J) {
+        double ca[CH][EPT], cb[CH][EPT];
+        load_rows<NT, EPT, CH>(c, path, 1 + hid * CH, J, ca);
+        for (int rb = hid; 1 + rb * CH <= J; rb += 2 * hps) {
+          load_rows<NT, EPT, CH>(c, path, 1 + (rb + hps) * CH, J, cb);
+          fma_rows<EPT, CH>(aw, R0, 1 + rb * CH, ca, acc);
+          if (1 + (rb + hps) * CH > J) break;
+          load_rows<NT, EPT, CH>(c, path, 1 + (rb + 2 * hps) * CH, J, ca);
+          fma_rows<EPT, CH>(aw, R0, 1 + (rb + hps) * CH, cb, acc);
         }
       }
 #pragma unroll
