@@ -121,6 +121,98 @@ __device__ __forceinline__ cd* fft_stockham(cd* a, cd* b, const cd* __restrict__
   return a;
 }
 
+// twiddle-table offset of radix-4 pass p (p >= 1)
+__host__ __device__ constexpr int tw_pass_offset(int p) {
+  int off = 0, ns = 4;
+  for (int q = 1; q < p; ++q, ns *= 4) off += 3 * ns;
+  return off;
+}
+
+// radix-4 Stockham passes [P0, P1) of a length-2^LG FFT (even LG), each ending with a barrier
+template <int LG, int NT, bool INV, int P0, int P1>
+__device__ __forceinline__ cd* fft_passes(cd* a, cd* b, const cd* __restrict__ twp) {
+  constexpr int L4 = (1 << LG) >> 2;
+#pragma unroll
+  for (int pass = P0; pass < P1; ++pass) {
+    const int Ns = 1 << (2 * pass);
+    const int off = tw_pass_offset(pass);
+#pragma unroll
+    for (int j0 = 0; j0 < L4; j0 += NT) {
+      const int j = j0 + (int)threadIdx.x;
+      if (L4 % NT == 0 || j < L4) {
+        const int k = j & (Ns - 1);
+        cd v0 = a[sw(j)], v1 = a[sw(j + L4)], v2 = a[sw(j + 2 * L4)], v3 = a[sw(j + 3 * L4)];
+        if (pass > 0) {
+          cd w1 = twp[off + k], w2 = twp[off + Ns + k], w3 = twp[off + 2 * Ns + k];
+          if (INV) {
+            w1.y = -w1.y;
+            w2.y = -w2.y;
+            w3.y = -w3.y;
+          }
+          v1 = cmul(v1, w1);
+          v2 = cmul(v2, w2);
+          v3 = cmul(v3, w3);
+        }
+        const cd t0 = cadd(v0, v2), t1 = csub(v0, v2), t2 = cadd(v1, v3), t3 = csub(v1, v3);
+        const cd mi3 = {t3.y, -t3.x};
+        const int base = ((j - k) << 2) + k;
+        b[sw(base)] = cadd(t0, t2);
+        b[sw(base + Ns)] = INV ? csub(t1, mi3) : cadd(t1, mi3);
+        b[sw(base + 2 * Ns)] = csub(t0, t2);
+        b[sw(base + 3 * Ns)] = INV ? cadd(t1, mi3) : csub(t1, mi3);
+      }
+    }
+    bar<NT>();
+    cd* t = a;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// Last radix-4 pass (Ns = L/4) of an inverse FFT kept in registers: thread j
+// owns outputs at positions j + r*L/4 (r = 0..3), which are exactly the inputs
+// of thread j in the first (Ns = 1) pass of a forward FFT.  Valid for even LG,
+// one butterfly per thread (L/4 <= NT).
+template <int LG>
+__device__ __forceinline__ void last_pass_inv_regs(const cd* a, const cd* __restrict__ twp, cd (&v)[4]) {
+  constexpr int L4 = (1 << LG) >> 2;
+  constexpr int P = LG / 2;
+  const int j = threadIdx.x;
+  v[0] = a[sw(j)];
+  v[1] = a[sw(j + L4)];
+  v[2] = a[sw(j + 2 * L4)];
+  v[3] = a[sw(j + 3 * L4)];
+  if (P > 1) {
+    const int off = tw_pass_offset(P - 1);
+    cd w1 = twp[off + j], w2 = twp[off + L4 + j], w3 = twp[off + 2 * L4 + j];
+    w1.y = -w1.y;
+    w2.y = -w2.y;
+    w3.y = -w3.y;
+    v[1] = cmul(v[1], w1);
+    v[2] = cmul(v[2], w2);
+    v[3] = cmul(v[3], w3);
+  }
+  const cd t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]), t2 = cadd(v[1], v[3]), t3 = csub(v[1], v[3]);
+  const cd mi3 = {t3.y, -t3.x};
+  v[0] = cadd(t0, t2);
+  v[1] = csub(t1, mi3);  // inverse: X1 = t1 + i t3
+  v[2] = csub(t0, t2);
+  v[3] = cadd(t1, mi3);
+}
+
+// First (Ns = 1, no twiddle) pass of a forward FFT from register inputs
+// x[r] = input position j + r*L/4; stores to b, no barrier.
+__device__ __forceinline__ void first_pass_fwd_regs(const cd (&x)[4], cd* b) {
+  const int j = threadIdx.x;
+  const cd t0 = cadd(x[0], x[2]), t1 = csub(x[0], x[2]), t2 = cadd(x[1], x[3]), t3 = csub(x[1], x[3]);
+  const cd mi3 = {t3.y, -t3.x};
+  b[sw(4 * j)] = cadd(t0, t2);
+  b[sw(4 * j + 1)] = cadd(t1, mi3);
+  b[sw(4 * j + 2)] = csub(t0, t2);
+  b[sw(4 * j + 3)] = csub(t1, mi3);
+}
+
 template <int NT, int EPT, int LG>
 struct Sine1D {
   static constexpr double SQ2 = 1.4142135623730951;
@@ -204,6 +296,15 @@ struct Sine1D {
     if (threadIdx.x == 0) A[0] = {0.0, 0.0};
   }
 
+  // even LG with one butterfly per thread: FFT boundary fused through registers
+  static constexpr bool kFuse = (LG % 2 == 0) && (LG >= 2) && ((1 << LG) / 4 <= NT);
+
+  // grid point of register slot r (position p = j + r*Q/4 of the synthesis output)
+  __device__ __forceinline__ static int qof(int j, int r) {
+    const int pos = j + r * (Q / 4);
+    return pos < Q / 2 ? 2 * pos : 2 * (Q - 1 - pos) + 1;
+  }
+
   // K p for owned modes (p, Kp in registers)
   __device__ __forceinline__ void apply_k(const double* p, double* kp) {
     double av[EPT], bv[EPT];
@@ -214,18 +315,34 @@ struct Sine1D {
     }
     synth_input(av, bv);
     bar<NT>();
-    cd* R = fft_stockham<LG, NT, true>(A, B, twp);
-    cd* O = (R == A) ? B : A;
+    cd* Z;
+    if constexpr (kFuse) {
+      constexpr int P = LG / 2;
+      cd* X = fft_passes<LG, NT, true, 0, P - 1>(A, B, twp);
+      cd* Y = (X == A) ? B : A;
+      if ((int)threadIdx.x < Q / 4) {
+        cd v[4];
+        last_pass_inv_regs<LG>(X, twp, v);
 #pragma unroll
-    for (int i = 0; i < QPT; ++i) {
-      const int q = threadIdx.x + i * NT;
-      if (Q % NT == 0 || q < Q) {
-        const int s = sw(perm(q));
-        R[s] = {0.0, dq[q] * (0.5 * R[s].y)};
+        for (int r = 0; r < 4; ++r) v[r] = {0.0, dq[qof(threadIdx.x, r)] * (0.5 * v[r].y)};
+        first_pass_fwd_regs(v, Y);
       }
+      bar<NT>();
+      Z = fft_passes<LG, NT, false, 1, P>(Y, X, twp);
+    } else {
+      cd* R = fft_stockham<LG, NT, true>(A, B, twp);
+      cd* O = (R == A) ? B : A;
+#pragma unroll
+      for (int i = 0; i < QPT; ++i) {
+        const int q = threadIdx.x + i * NT;
+        if (Q % NT == 0 || q < Q) {
+          const int s = sw(perm(q));
+          R[s] = {0.0, dq[q] * (0.5 * R[s].y)};
+        }
+      }
+      bar<NT>();
+      Z = fft_stockham<LG, NT, false>(R, O, twp);
     }
-    bar<NT>();
-    cd* Z = fft_stockham<LG, NT, false>(R, O, twp);
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int k = mode(i);
@@ -235,6 +352,32 @@ struct Sine1D {
         const double Dx = a.x - b.x, Dy = a.y + b.y;
         kp[i] = SQ2 * CUDART_PI * (double)k * (0.5 * (c.x * Dy - c.y * Dx));
       }
+    }
+  }
+
+  // fused setup pointwise on the register slots (kFuse path): v[r] holds the
+  // synthesis output at grid point qof(j, r); returns analysis inputs in v
+  template <int FID>
+  __device__ __forceinline__ void pointwise_regs(const Fn& fn, cd (&v)[4], double t, double emt, double& dsum,
+                                                 double& nbad, int& bad) {
+    const double wq = 1.0 / (double)Q;
+    Fn f1 = fn;
+    if (FID != 0) f1.id = FID;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int q = qof(threadIdx.x, r);
+      const double s1 = 0.5 * v[r].x, s2 = 0.5 * v[r].y;
+      const double u = (q & 1) ? -s1 : s1;
+      const double Dv = fn_D(f1, xq[q], 0.0, t, u);
+      if (!isfinite(Dv)) {
+        bad = min(bad, q);
+        nbad += 1.0;
+      }
+      const double d = wq * Dv;
+      const double g = wq * fn_f(f1, xtab[q], emt, u);
+      dq[q] = d;
+      dsum += d;
+      v[r] = {(q & 1) ? -g : g, d * s2};
     }
   }
 
@@ -284,31 +427,58 @@ struct Sine1D {
       synth_input(av, bv);
     }
     bar<NT>();
-    cd* R = fft_stockham<LG, NT, true>(A, B, twp);
-    cd* O = (R == A) ? B : A;
-    PF_T(1);
-    // --- pointwise coefficients (fused epilogue) ------------------------
     const double emt = fn.id == 1 ? exp(-t) : 0.0;  // only PF_FN_POLY's source uses exp(-t)
-    double dsum = 0.0, nbad = 0.0;
+    double dsum = 0.0, nbad = 0.0, dbar = 0.0;
     int bad = 0x7fffffff;
-    // one switch outside the point loop: each functor's loop is straight-line
-    // code, so the compiler interleaves the QPT transcendental evaluations
-    switch (fn.id) {
-      case 1: pointwise<1>(fn, R, t, emt, dsum, nbad, bad); break;
-      case 2: pointwise<2>(fn, R, t, emt, dsum, nbad, bad); break;
-      case 3: pointwise<3>(fn, R, t, emt, dsum, nbad, bad); break;
-      case 4: pointwise<4>(fn, R, t, emt, dsum, nbad, bad); break;
-      default: pointwise<0>(fn, R, t, emt, dsum, nbad, bad); break;
+    cd* Z;
+    if constexpr (kFuse) {
+      constexpr int P = LG / 2;
+      cd* X = fft_passes<LG, NT, true, 0, P - 1>(A, B, twp);
+      cd* Y = (X == A) ? B : A;
+      PF_T(1);
+      if ((int)threadIdx.x < Q / 4) {
+        cd v[4];
+        last_pass_inv_regs<LG>(X, twp, v);
+        switch (fn.id) {
+          case 1: pointwise_regs<1>(fn, v, t, emt, dsum, nbad, bad); break;
+          case 2: pointwise_regs<2>(fn, v, t, emt, dsum, nbad, bad); break;
+          case 3: pointwise_regs<3>(fn, v, t, emt, dsum, nbad, bad); break;
+          case 4: pointwise_regs<4>(fn, v, t, emt, dsum, nbad, bad); break;
+          default: pointwise_regs<0>(fn, v, t, emt, dsum, nbad, bad); break;
+        }
+        first_pass_fwd_regs(v, Y);
+      }
+      const double2 s01 = red.sum2(dsum, nbad);  // barrier: orders the first pass too
+      if (s01.y > 0.0) {
+        st.node = red.min_int(bad);
+        return ST_COEFF;
+      }
+      dbar = s01.x;
+      PF_T(2);
+      Z = fft_passes<LG, NT, false, 1, P>(Y, X, twp);
+    } else {
+      cd* R = fft_stockham<LG, NT, true>(A, B, twp);
+      cd* O = (R == A) ? B : A;
+      PF_T(1);
+      // one switch outside the point loop: each functor's loop is straight-line
+      // code, so the compiler interleaves the QPT transcendental evaluations
+      switch (fn.id) {
+        case 1: pointwise<1>(fn, R, t, emt, dsum, nbad, bad); break;
+        case 2: pointwise<2>(fn, R, t, emt, dsum, nbad, bad); break;
+        case 3: pointwise<3>(fn, R, t, emt, dsum, nbad, bad); break;
+        case 4: pointwise<4>(fn, R, t, emt, dsum, nbad, bad); break;
+        default: pointwise<0>(fn, R, t, emt, dsum, nbad, bad); break;
+      }
+      const double2 s01 = red.sum2(dsum, nbad);
+      if (s01.y > 0.0) {
+        st.node = red.min_int(bad);
+        return ST_COEFF;
+      }
+      dbar = s01.x;
+      PF_T(2);
+      // --- analysis pair: F = S^T g, K x0 = S'^T (d v0) --------------------
+      Z = fft_stockham<LG, NT, false>(R, O, twp);
     }
-    const double2 s01 = red.sum2(dsum, nbad);
-    if (s01.y > 0.0) {
-      st.node = red.min_int(bad);
-      return ST_COEFF;
-    }
-    const double dbar = s01.x;
-    PF_T(2);
-    // --- analysis pair: F = S^T g, K x0 = S'^T (d v0) --------------------
-    cd* Z = fft_stockham<LG, NT, false>(R, O, twp);
     PF_T(3);
     double x[EPT], r[EPT], p[EPT], z[EPT], pinv[EPT];
     double bb = 0.0, rr = 0.0, rzl = 0.0;
