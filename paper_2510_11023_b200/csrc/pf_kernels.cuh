@@ -464,9 +464,12 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
 
 // coarse step G(H[0..n]) -> x  (stepping.py:87-112)
 template <class SP, int NT, int EPT>
+// PCG guess: kind 0 -> U_n; 1 -> 2 U_n - U_{n-1} (run_coarse); 2 -> G_old[n] + (U_next[n] - U_cur[n])
+// (correction sweep: the previous sweep's coarse step of the slightly different state)
 __device__ __forceinline__ int coarse_apply(SP& sp, const Common& c, const double* H, int n, double* xout,
-                                            Status& st) {
-  double h[EPT], z[EPT], xp[EPT];
+                                            Status& st, int guess = 0, const double* gold = nullptr,
+                                            const double* ucur = nullptr) {
+  double h[EPT], z[EPT], xp[EPT], xg[EPT];
   const double* __restrict__ b = c.bfine;
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
@@ -480,8 +483,11 @@ __device__ __forceinline__ int coarse_apply(SP& sp, const Common& c, const doubl
       h[i] = acc;
       xp[i] = H[(size_t)n * c.size + e];
     }
+    xg[i] = xp[i];
+    if (e < c.size && guess == 1 && n >= 1) xg[i] = fma(2.0, xp[i], -H[(size_t)(n - 1) * c.size + e]);
+    if (e < c.size && guess == 2) xg[i] = gold[(size_t)n * c.size + e] + (xp[i] - ucur[(size_t)n * c.size + e]);
   }
-  return sp.step(c.fn, xp, xp, (double)n * c.dT, c.gam_c, h, z, xout, st);
+  return sp.step(c.fn, xp, xg, (double)n * c.dT, c.gam_c, h, z, xout, st);
 }
 
 enum CoarseMode : int { CM_RUN = 0, CM_CORRECT = 1, CM_SINGLE = 2 };
@@ -522,7 +528,7 @@ __global__ void __launch_bounds__(NT) k_coarse(Common c, SPP spp, CoarseArgs a, 
   } else if (a.mode == CM_RUN) {
     for (int n = 0; n < c.nt; ++n) {
       st.n = n;
-      const int code = coarse_apply<SP, NT, EPT>(sp, c, a.traj, n, x, st);
+      const int code = coarse_apply<SP, NT, EPT>(sp, c, a.traj, n, x, st, 1);
       if (code != ST_OK) {
         st.code = code;
         break;
@@ -541,7 +547,7 @@ __global__ void __launch_bounds__(NT) k_coarse(Common c, SPP spp, CoarseArgs a, 
     }
     for (int n = 0; n < c.nt; ++n) {
       st.n = n;
-      const int code = coarse_apply<SP, NT, EPT>(sp, c, a.unext, n, x, st);
+      const int code = coarse_apply<SP, NT, EPT>(sp, c, a.unext, n, x, st, 2, a.gold, a.ucur);
       if (code != ST_OK) {
         st.code = code;
         break;
