@@ -173,6 +173,11 @@ int pf_dev_parareal_init(pf_ctx* ctx, const double* u0);
 const double* pf_dev_parareal_states(pf_ctx* ctx); /* device pointer, (nt+1) rows */
 int pf_dev_parareal_correct(pf_ctx* ctx, const double* d_fold, int k, double* diff);
 int pf_dev_parareal_read(pf_ctx* ctx, double* states, double* coarse_new, double* coarse_old);
+/* Leading nodes the last correction left bitwise unchanged (0 before the
+ * first).  Slices below it have exactly the inputs of their previous fine
+ * sweep, so their F_old rows stand and the next sweep may start there --
+ * parareal's finite termination (parareal.py:114-118, 175-189) made exact. */
+int pf_dev_parareal_frozen(pf_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -88,6 +88,7 @@ SIGNATURES = {
     "pf_dev_parareal_states": (C.c_void_p, [C.c_void_p]),
     "pf_dev_parareal_correct": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _dp]),
     "pf_dev_parareal_read": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
+    "pf_dev_parareal_frozen": (C.c_int, [C.c_void_p]),
 }
 
 

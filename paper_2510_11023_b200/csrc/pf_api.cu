@@ -81,6 +81,7 @@ struct pf_ctx {
   pf_error err{};
   double guard = 0;
   bool parareal_ready = false;
+  int frozen = 0;  // leading nodes the last correction left bitwise unchanged
   int pending_lo = -1, pending_bs = 0;  // last async fine launch, decoded by pf_dev_check
   int* d_sync = nullptr;                 // sweep progress / ready / abort flags
   int sync_cap = 0;
@@ -809,10 +810,13 @@ int pf_dev_parareal_init(pf_ctx* c, const double* u0) {
   PF_CUDA(c, cudaMemcpyAsync(c->gold.p, c->U.p + sz, (rows - 1) * sz * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   c->guard = 1e12 * std::max(host_norm(c, u0), 1.0);  // parareal.py:98
   c->parareal_ready = true;
+  c->frozen = 0;
   return 0;
 }
 
 const double* pf_dev_parareal_states(pf_ctx* c) { return c ? c->U.p : nullptr; }
+
+int pf_dev_parareal_frozen(pf_ctx* c) { return c ? c->frozen : 0; }
 
 int pf_dev_parareal_correct(pf_ctx* c, const double* d_fold, int k, double* diff) {
   if (!c || !c->parareal_ready) return c ? set_error(c, PF_ERR_ARGUMENT, "parareal state not initialised") : PF_ERR_ARGUMENT;
@@ -847,12 +851,13 @@ int pf_dev_parareal_correct(pf_ctx* c, const double* d_fold, int k, double* diff
   int rc = launch_coarse(c, a, c->d_status);
   if (rc) return rc;
   PF_CUDA(c, cudaEventRecord(c->ev1, c->stream));
-  double h = 0.0;
-  PF_CUDA(c, cudaMemcpyAsync(&h, c->scalar.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  double h[2] = {0.0, 0.0};
+  PF_CUDA(c, cudaMemcpyAsync(h, c->scalar.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   rc = decode_coarse(c, 0, k);
   if (cudaEventElapsedTime(&ms, c->ev0, c->ev1) == cudaSuccess) c->stats.last_coarse_ms = ms;
   if (rc) return rc;
-  if (diff) *diff = h;
+  if (diff) *diff = h[0];
+  c->frozen = std::min((int)h[1], c->grid.nt);
   std::swap(c->U, c->Unext);  // u_curr = u_next (parareal.py:133)
   return 0;
 }
@@ -886,8 +891,13 @@ int pf_parareal(pf_ctx* c, const double* u0, double tol, int k_max, const double
   }
   int iters = 0, stop = 0;
   for (int k = 0; k < k_max; ++k) {
-    rc = pf_dev_fine_sweep(c, c->U.p, 0, nt, c->fold.p);
-    if (rc) return rc;
+    // slices below the frozen prefix have bitwise the inputs of their last
+    // sweep: their F_old rows stand (see k_coarse CM_CORRECT)
+    const int lo = k == 0 ? 0 : c->frozen;
+    if (lo < nt) {
+      rc = pf_dev_fine_sweep(c, c->U.p, lo, nt, c->fold.p + (size_t)lo * sz);
+      if (rc) return rc;
+    }
     double diff = 0.0;
     rc = pf_dev_parareal_correct(c, c->fold.p, k, &diff);
     if (rc) return rc;

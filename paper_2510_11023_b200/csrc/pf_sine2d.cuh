@@ -862,21 +862,33 @@ __global__ void k2_correct_row(const double* fold, const double* gnew, const dou
     unext[e] = fold[e] + (gnew[e] - gold[e]);
 }
 
-// node norms / diff for the guards (parareal.py:120-128): one CTA per node, fixed order
-__global__ void k2_node_norms(const double* unext, const double* ucur, long MM, double* out /* (nt+1, 3) */) {
+// any bitwise difference between two states -> *flag = 1
+__global__ void k2_differs(const double* a, const double* b, long MM, int* flag) {
+  int d = 0;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < (size_t)MM; e += (size_t)gridDim.x * blockDim.x)
+    d |= __double_as_longlong(a[e]) != __double_as_longlong(b[e]);
+  if (__syncthreads_or(d) && threadIdx.x == 0) *flag = 1;
+}
+
+// node norms / diff for the guards (parareal.py:120-128): one CTA per node,
+// fixed order; out[4n+3] = 1 when the node is bitwise unchanged
+__global__ void k2_node_norms(const double* unext, const double* ucur, long MM, double* out /* (nt+1, 4) */) {
   const int n = blockIdx.x;
   __shared__ double red[2 * 256];
   double s0 = 0.0, s1 = 0.0;
-  int fin = 1;
+  int fin = 1, eq = 1;
   for (size_t e = threadIdx.x; e < (size_t)MM; e += blockDim.x) {
     const double v = unext[(size_t)n * MM + e];
-    const double d = v - ucur[(size_t)n * MM + e];
+    const double u = ucur[(size_t)n * MM + e];
+    const double d = v - u;
     if (!isfinite(v)) fin = 0;
+    eq &= __double_as_longlong(v) == __double_as_longlong(u);
     s0 = fma(v, v, s0);
     s1 = fma(d, d, s1);
   }
   red[2 * threadIdx.x] = s0;
   red[2 * threadIdx.x + 1] = s1;
+  const int alleq = __syncthreads_and(eq);
   const int allfin = __syncthreads_and(fin);
   if (threadIdx.x == 0) {
     double a = 0.0, c = 0.0;
@@ -884,9 +896,10 @@ __global__ void k2_node_norms(const double* unext, const double* ucur, long MM, 
       a += red[2 * i];
       c += red[2 * i + 1];
     }
-    out[3 * n] = sqrt(a);
-    out[3 * n + 1] = sqrt(c);
-    out[3 * n + 2] = allfin ? 1.0 : 0.0;
+    out[4 * n] = sqrt(a);
+    out[4 * n + 1] = sqrt(c);
+    out[4 * n + 2] = allfin ? 1.0 : 0.0;
+    out[4 * n + 3] = alleq ? 1.0 : 0.0;
   }
 }
 

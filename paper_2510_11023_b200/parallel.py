@@ -74,6 +74,10 @@ class DeviceOps:
         self.ctx.check(L.lib.pf_dev_fine_sweep(self.ctx.handle, L.C.c_void_p(states), lo, hi,
                                                L.C.c_void_p(out.data_ptr())))
 
+    def frozen(self):
+        """Leading nodes the last correction left bitwise unchanged."""
+        return int(self._lib.lib.pf_dev_parareal_frozen(self.ctx.handle))
+
     def correct(self, fold_all, k):
         L = self._lib
         diff = L.C.c_double(0.0)
@@ -131,8 +135,11 @@ class DistributedParareal:
         diffs, times, fold = [], [], None
         stop_reason, iterations = "k_max", 0
         for k in range(k_max):
-            if hi > lo:
-                self.ops.fine(lo, hi, local)
+            # slices below the frozen prefix keep their F_old rows (their inputs
+            # are bitwise those of their last sweep): finite termination made exact
+            start = lo if k == 0 else max(lo, min(hi, self.ops.frozen()))
+            if hi > start:
+                self.ops.fine(start, hi, local[start - lo:])
             fold = self.gather(local)
             diff = self.ops.correct(fold, k)
             diffs.append(diff)

@@ -3,7 +3,8 @@
 The GPU ranks run the sm_100a sweep; here each rank runs the oracle sweep on
 CPU tensors behind the same ops interface, so the sharding
 (parareal._block_bounds, parareal.py:62-72), the padded all-gather with
-uneven blocks, the G_old reuse and the replicated correction sweep are
+uneven blocks, the G_old reuse, the frozen-prefix skip of unchanged slices
+and the replicated correction sweep are
 checked for world_size 2 and 3 against the single-process oracle —
 iterates must agree bitwise (the rank-count analogue of the reference's
 thread-count invariance, test_parareal.py:128-138).
@@ -28,9 +29,13 @@ class OracleOps:
 
     torch = torch
 
-    def __init__(self, problem, space, grids):
+    def __init__(self, problem, space, grids, block_lo=0):
         self.problem, self.space, self.grids = problem, space, grids
         self.size = space.size
+        # the oracle's batched numpy sweep is not bitwise batch-composition
+        # invariant (the device kernel is: one CTA per slice), so a partial
+        # sweep [lo, hi) recomputes the rank's whole block and keeps the tail
+        self.block_lo = block_lo
 
     def empty(self, rows):
         return torch.empty((rows, self.size), dtype=torch.float64)
@@ -42,8 +47,9 @@ class OracleOps:
         self.k = -1
 
     def fine(self, lo, hi, out):
-        out[: hi - lo] = torch.from_numpy(
-            oracle.fine_sweep_intervals(self.U, lo, hi, self.space, self.grids, self.problem))
+        self.swept = getattr(self, "swept", 0) + (hi - lo)
+        full = oracle.fine_sweep_intervals(self.U, self.block_lo, hi, self.space, self.grids, self.problem)
+        out[: hi - lo] = torch.from_numpy(full[lo - self.block_lo:])
 
     def correct(self, fold_all, k):
         if k > 0:
@@ -55,8 +61,13 @@ class OracleOps:
             self.gnew[n] = oracle.coarse_step(nxt[: n + 1], self.space, self.grids, self.problem, step_index=n)
             nxt[n + 1] = fold[n] + (self.gnew[n] - self.gold[n])
         diff = max(self.space.norm(nxt[n] - self.U[n]) for n in range(self.grids.nt + 1))
+        same = [np.array_equal(nxt[n].view(np.int64), self.U[n].view(np.int64)) for n in range(self.grids.nt + 1)]
+        self.first_changed = same.index(False) if False in same else self.grids.nt
         self.U = nxt
         return diff
+
+    def frozen(self):
+        return self.first_changed
 
     def read(self):
         return self.U, self.gnew, self.gold
@@ -73,9 +84,10 @@ def _worker(rank, world, port, nt, out_q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         prob = P.config(1, modes=8)
-        ops = OracleOps(prob, oracle.Sine1D(8), oracle.TimeGrids(1.0, nt, 4))
+        ops = OracleOps(prob, oracle.Sine1D(8), oracle.TimeGrids(1.0, nt, 4), block_bounds(nt, world)[rank][0])
         res = DistributedParareal(ops, nt).solve(tol=1e-12, k_max=nt + 1)
-        out_q.put((rank, res["states"], res["diffs"], res["k"], res["coarse_old"], res["fine_endpoints"]))
+        out_q.put((rank, res["states"], res["diffs"], res["k"], res["coarse_old"], res["fine_endpoints"],
+                   getattr(ops, "swept", 0)))
     finally:
         dist.destroy_process_group()
 
@@ -95,12 +107,16 @@ def test_distributed_matches_single_process(world, nt):
     prob = P.config(1, modes=8)
     sp = oracle.Sine1D(8)
     it, rep = oracle.solve(prob, sp, oracle.TimeGrids(1.0, nt, 4), tol=1e-12, k_max=nt + 1)
-    for rank, states, diffs, k, g_old, f_old in results:
+    swept = 0
+    for rank, states, diffs, k, g_old, f_old, sw in results:
+        swept += sw
         assert k == rep.iterations
         np.testing.assert_array_equal(states, it.states)
         np.testing.assert_array_equal(g_old, it.coarse_old)
         np.testing.assert_array_equal(f_old, it.fine_endpoints)
         assert diffs == rep.diffs
+    # iteration k re-sweeps only slices k..nt-1 (the frozen prefix is skipped)
+    assert swept == sum(nt - k for k in range(rep.iterations)), (swept, rep.iterations)
 
 
 def test_uneven_bounds_cover_all_ranks():

@@ -1,0 +1,92 @@
+"""Copy one round_evidence.sh run (gpurun_out/*_TAG*) into profiles/ as the
+judged summaries: bench lines, the ncu launch list (per-kernel shares), the
+raw metrics + top stall lines of the --set full capture, phase / per-slice
+breakdowns, the GPU test log, and dram_config3.json (roofline.traffic).
+
+    python tools/collect_evidence.py r01c
+"""
+import collections
+import csv
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+G = os.path.join(ROOT, "gpurun_out")
+P = os.path.join(ROOT, "profiles")
+RAW = ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+       "gpu__time_duration.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__block_size",
+       "launch__grid_size", "launch__registers_per_thread", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+       "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+       "smsp__inst_executed.sum", "smsp__pcsamp_warps_issue_stalled_barrier",
+       "smsp__pcsamp_warps_issue_stalled_long_scoreboard", "smsp__pcsamp_warps_issue_stalled_short_scoreboard",
+       "smsp__pcsamp_warps_issue_stalled_wait", "smsp__pcsamp_warps_issue_stalled_mio_throttle",
+       "smsp__pcsamp_warps_issue_stalled_math_pipe_throttle", "smsp__pcsamp_warps_issue_stalled_no_instructions")
+
+
+def main(tag):
+    for src, dst in (("bench", "bench"), ("bench_ref", "bench_ref"), ("bench_c2", "bench_c2"), ("bench_c4", "bench_c4")):
+        f = os.path.join(G, f"{src}_{tag}.json")
+        if os.path.exists(f):
+            shutil.copy(f, os.path.join(P, f"{tag}_{dst}.json"))
+    for src, dst in (("pytest_gpu", "pytest_gpu.txt"), ("phases", "phases_slice0_config3.txt"),
+                     ("slices", "per_slice_config3.txt"), ("smoke", "smoke.txt")):
+        f = os.path.join(G, f"{src}_{tag}.txt")
+        if os.path.exists(f):
+            shutil.copy(f, os.path.join(P, f"{tag}_{dst}"))
+    # launch list
+    lines = open(os.path.join(G, f"launches_{tag}.csv")).read().splitlines()
+    start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
+    rows = list(csv.reader(lines[start:]))
+    h = rows[0]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = collections.OrderedDict()
+    tot = 0.0
+    for r in rows[1:]:
+        k = r[ki].split("(")[0]
+        v = float(r[vi].replace(",", ""))
+        agg.setdefault(k, []).append(v)
+        tot += v
+    with open(os.path.join(P, f"{tag}_launch_list.txt"), "w") as f:
+        f.write("# ncu --metrics gpu__time_duration.sum --clock-control none  "
+                "python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-parareal\n")
+        f.write("# cold-cache, serialised launches (compare shares, not absolutes); the timed step is one "
+                "k_fine_sweep launch;\n# k_coarse is the untimed run_coarse that prepares the inputs; the "
+                "remaining time is torch's own fill/copy kernels.\n")
+        for k, vs in agg.items():
+            f.write(f"{len(vs):4d} x {sum(vs) / len(vs) / 1e6:9.3f} ms  {100 * sum(vs) / tot:5.1f}%  {k}\n")
+    # full capture
+    rep = os.path.join(G, f"prof_{tag}.ncu-rep")
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(raw.splitlines()))
+    names, units, vals = rr[0], rr[1], rr[2]
+    out = {}
+    with open(os.path.join(P, f"{tag}_ncu_full_fine_sweep_raw.txt"), "w") as f:
+        f.write(f"# ncu --set full --clock-control none -k regex:k_fine_sweep -c 1 (config 3), gpurun_out/prof_{tag}.ncu-rep\n")
+        for m in RAW:
+            if m in names:
+                i = names.index(m)
+                out[m] = vals[i]
+                f.write(f"{m:70s} {vals[i]} {units[i]}\n")
+    det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    open(os.path.join(P, f"{tag}_ncu_full_fine_sweep_details.csv"), "w").write(det)
+    hot = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_top.py"), rep, "40"],
+                         capture_output=True, text=True).stdout
+    open(os.path.join(P, f"{tag}_ncu_full_fine_sweep_hotlines.txt"), "w").write(hot)
+
+    def nbytes(m):
+        i = names.index(m)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[units[i]]
+        return float(vals[i].replace(",", "")) * scale
+
+    traffic = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
+    json.dump({"dram_bytes_per_launch": int(traffic),
+               "source": f"ncu --set full, gpurun_out/prof_{tag}.ncu-rep (dram__bytes_read.sum + dram__bytes_write.sum)",
+               "config": 3}, open(os.path.join(P, "dram_config3.json"), "w"), indent=1)
+    print("traffic", traffic, "launches", {k: len(v) for k, v in agg.items()})
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
