@@ -184,6 +184,43 @@ __device__ __forceinline__ cd* fft_lines_reg(cd* a, cd* b, const TwReg<LG>& tr, 
   return a;
 }
 
+// Radix-4 passes [P0, P1) of fft_lines_reg (even LG, TPL == L/4), each ending
+// with a barrier.
+template <int LG, bool INV, int P0, int P1>
+__device__ __forceinline__ cd* fft_lines_reg_passes(cd* a, cd* b, const TwReg<LG>& tr, int lane) {
+  constexpr int L4 = (1 << LG) >> 2;
+#pragma unroll
+  for (int pass = P0; pass < P1; ++pass) {
+    const int Ns = 1 << (2 * pass);
+    const int j = lane;
+    const int k = j & (Ns - 1);
+    cd v0 = a[sw(j)], v1 = a[sw(j + L4)], v2 = a[sw(j + 2 * L4)], v3 = a[sw(j + 3 * L4)];
+    if (pass > 0) {
+      cd w1 = tr.w[pass][0], w2 = tr.w[pass][1], w3 = tr.w[pass][2];
+      if (INV) {
+        w1.y = -w1.y;
+        w2.y = -w2.y;
+        w3.y = -w3.y;
+      }
+      v1 = cmul(v1, w1);
+      v2 = cmul(v2, w2);
+      v3 = cmul(v3, w3);
+    }
+    const cd t0 = cadd(v0, v2), t1 = csub(v0, v2), t2 = cadd(v1, v3), t3 = csub(v1, v3);
+    const cd mi3 = {t3.y, -t3.x};
+    const int base = ((j - k) << 2) + k;
+    b[sw(base)] = cadd(t0, t2);
+    b[sw(base + Ns)] = INV ? csub(t1, mi3) : cadd(t1, mi3);
+    b[sw(base + 2 * Ns)] = csub(t0, t2);
+    b[sw(base + 3 * Ns)] = INV ? cadd(t1, mi3) : csub(t1, mi3);
+    __syncthreads();
+    cd* t = a;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
 // line FFT dispatch: register twiddles when every lane owns one butterfly per pass
 template <int LG, int TPL, bool INV>
 __device__ __forceinline__ cd* line_fft(cd* a, cd* b, const TwReg<LG>& tr, const cd* __restrict__ twp, int lane) {
@@ -373,9 +410,181 @@ __global__ void __launch_bounds__(256) k2_cols(Sine2DArgs a) {
   const bool live = line < L::TL && q2 < L::Q;
   const size_t hl = ((size_t)b * L::Q + q2) * L::M;  // H line base [b][q2][.]
   const size_t gl = ((size_t)b * L::Q + q2) * L::Q;  // grid line base [b][q2][.]
+  if constexpr (!SETUP && (LG % 2 == 0) && L::TPL == L::Q / 4 && LG >= 4) {
+    // CG matvec, fused: the synthesis FFT's last pass, the pointwise scaling
+    // and the analysis FFT's first pass stay in registers.  For the pair
+    // (a = sqrt2 Hc, b = sqrt2 pi k1 Hs) the pointwise map at FFT position j
+    // (grid point q(j) of the Makhoul reorder) is Z_j = (0.5 d_q) W_j: the
+    // sin part (Gy) and cos part (Gx) are both scaled by d, the sign of the
+    // odd points cancels between extraction and re-insertion.
+    constexpr int P = LG / 2, L4 = L::Q / 4;
+    cd* W = A + line * L::Q;
+    if (live) {
+      if (lane == 0) W[0] = {0.0, 0.0};
+      for (int k = lane + 1; k <= L::M; k += L::TPL)
+        synth_write<LG>(W, ph, k, L::SQ2 * a.Hc[hl + k - 1], L::SQ2 * CUDART_PI * (double)k * a.Hs[hl + k - 1]);
+    }
+    __syncthreads();
+    cd* X = fft_lines_reg_passes<LG, true, 0, P - 1>(A + line * L::Q, B + line * L::Q, tr, lane);
+    cd* Y = (X == A + line * L::Q) ? B + line * L::Q : A + line * L::Q;
+    {
+      const int j = lane;
+      cd v[4];
+      double dv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int pos = j + r * L4;
+        const int q = pos < L::Q / 2 ? 2 * pos : 2 * (L::Q - 1 - pos) + 1;
+        dv[r] = live ? 0.5 * a.D[gl + q] : 0.0;
+        v[r] = X[sw(pos)];
+      }
+      cd w1 = tr.w[P - 1][0], w2 = tr.w[P - 1][1], w3 = tr.w[P - 1][2];
+      w1.y = -w1.y;
+      w2.y = -w2.y;
+      w3.y = -w3.y;
+      v[1] = cmul(v[1], w1);
+      v[2] = cmul(v[2], w2);
+      v[3] = cmul(v[3], w3);
+      const cd t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]), t2 = cadd(v[1], v[3]), t3 = csub(v[1], v[3]);
+      const cd mi3 = {t3.y, -t3.x};
+      cd x[4] = {cadd(t0, t2), csub(t1, mi3), csub(t0, t2), cadd(t1, mi3)};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) x[r] = {dv[r] * x[r].x, dv[r] * x[r].y};
+      const cd u0 = cadd(x[0], x[2]), u1 = csub(x[0], x[2]), u2 = cadd(x[1], x[3]), u3 = csub(x[1], x[3]);
+      const cd mu3 = {u3.y, -u3.x};
+      Y[sw(4 * j)] = cadd(u0, u2);
+      Y[sw(4 * j + 1)] = cadd(u1, mu3);
+      Y[sw(4 * j + 2)] = csub(u0, u2);
+      Y[sw(4 * j + 3)] = csub(u1, mu3);
+    }
+    __syncthreads();
+    cd* Zl = fft_lines_reg_passes<LG, false, 1, P>(Y, X, tr, lane);
+    if (live) {
+      for (int k = lane + 1; k <= L::M; k += L::TPL) {
+        const double2 Xv = anal_read(Zl, ph, L::Q, k);
+        a.Ay[hl + k - 1] = L::SQ2 * Xv.x;
+        a.Ax[hl + k - 1] = L::SQ2 * CUDART_PI * (double)k * Xv.y;
+      }
+    }
+    return;
+  }
   const double wq = 1.0 / ((double)L::Q * (double)L::Q);
   const double t = (double)(a.n0 + b) * a.dTs + a.tr;
   const double emt = a.fn.id == 1 ? exp(-t) : 0.0;
+  if constexpr (SETUP && (LG % 2 == 0) && L::TPL == L::Q / 4 && LG >= 4) {
+    // setup, fused: the last passes of the two synthesis FFTs end in
+    // registers, the coefficients are evaluated there, and the two analysis
+    // FFTs start from registers (same arithmetic as the staged path below,
+    // except the order of the per-lane dbar partial sums).
+    constexpr int P = LG / 2, L4 = L::Q / 4;
+    cd* A0 = A + line * L::Q;
+    cd* B0 = B + line * L::Q;
+    auto last_inv = [&](const cd* X, cd (&v)[4]) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) v[r] = X[sw(lane + r * L4)];
+      cd w1 = tr.w[P - 1][0], w2 = tr.w[P - 1][1], w3 = tr.w[P - 1][2];
+      w1.y = -w1.y;
+      w2.y = -w2.y;
+      w3.y = -w3.y;
+      v[1] = cmul(v[1], w1);
+      v[2] = cmul(v[2], w2);
+      v[3] = cmul(v[3], w3);
+      const cd t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]), t2 = cadd(v[1], v[3]), t3 = csub(v[1], v[3]);
+      const cd mi3 = {t3.y, -t3.x};
+      v[0] = cadd(t0, t2);
+      v[1] = csub(t1, mi3);
+      v[2] = csub(t0, t2);
+      v[3] = cadd(t1, mi3);
+    };
+    auto first_fwd = [&](const cd (&x)[4], cd* Y) {
+      const cd u0 = cadd(x[0], x[2]), u1 = csub(x[0], x[2]), u2 = cadd(x[1], x[3]), u3 = csub(x[1], x[3]);
+      const cd mu3 = {u3.y, -u3.x};
+      Y[sw(4 * lane)] = cadd(u0, u2);
+      Y[sw(4 * lane + 1)] = cadd(u1, mu3);
+      Y[sw(4 * lane + 2)] = csub(u0, u2);
+      Y[sw(4 * lane + 3)] = csub(u1, mu3);
+    };
+    // FFT1: (sqrt2 Hu, sqrt2 pi k1 Hs) -> u (sin), Gx (cos)
+    if (live) {
+      if (lane == 0) A0[0] = {0.0, 0.0};
+      for (int k = lane + 1; k <= L::M; k += L::TPL)
+        synth_write<LG>(A0, ph, k, L::SQ2 * a.Hu[hl + k - 1], L::SQ2 * CUDART_PI * (double)k * a.Hs[hl + k - 1]);
+    }
+    __syncthreads();
+    cd* X1 = fft_lines_reg_passes<LG, true, 0, P - 1>(A0, B0, tr, lane);
+    cd* Y1 = (X1 == A0) ? B0 : A0;  // free: its data was consumed before the last barrier
+    cd v1[4];
+    last_inv(X1, v1);
+    // FFT2: (sqrt2 Hc, 0) -> Gy (sin), staged in the free buffer
+    if (live) {
+      if (lane == 0) Y1[0] = {0.0, 0.0};
+      for (int k = lane + 1; k <= L::M; k += L::TPL) synth_write<LG>(Y1, ph, k, L::SQ2 * a.Hc[hl + k - 1], 0.0);
+    }
+    __syncthreads();
+    cd* X2 = fft_lines_reg_passes<LG, true, 0, P - 1>(Y1, X1, tr, lane);
+    cd* Y2 = (X2 == A0) ? B0 : A0;
+    cd v2[4];
+    last_inv(X2, v2);
+    // pointwise at grid point q(pos) of each register position
+    cd x3[4], x4[4];
+    double dsum = 0.0;
+    int bad = 0x7fffffff;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int pos = lane + r * L4;
+      const int q1 = pos < L::Q / 2 ? 2 * pos : 2 * (L::Q - 1 - pos) + 1;
+      const double u = (q1 & 1) ? -0.5 * v1[r].x : 0.5 * v1[r].x;
+      const double gx = 0.5 * v1[r].y;
+      const double gy = (q1 & 1) ? -0.5 * v2[r].x : 0.5 * v2[r].x;
+      x3[r] = {0.0, 0.0};
+      x4[r] = {0.0, 0.0};
+      if (live) {
+        const double x1 = a.xq[q1];
+        const double Dv = fn_D(a.fn, x1, a.xq[q2], t, u);
+        if (!isfinite(Dv)) bad = min(bad, q2 * L::Q + q1);
+        const double d = wq * Dv;
+        const double g = wq * (a.fn.id == 4 ? fn_f(a.fn, make_double2(0.0, 0.0), emt, u)
+                                            : fn_f(a.fn, fn_xtab(x1), emt, u));
+        a.D[gl + q1] = d;
+        dsum += d;
+        const double sp3 = g, cp3 = d * gx, sp4 = d * gy;
+        x3[r] = {(q1 & 1) ? -sp3 : sp3, cp3};
+        x4[r] = {(q1 & 1) ? -sp4 : sp4, 0.0};
+      }
+    }
+    // FFT3: (g, Yx) -> Ag, Ax
+    first_fwd(x3, Y2);
+    __syncthreads();
+    cd* Z3 = fft_lines_reg_passes<LG, false, 1, P>(Y2, X2, tr, lane);
+    if (live) {
+      for (int k = lane + 1; k <= L::M; k += L::TPL) {
+        const double2 Xv = anal_read(Z3, ph, L::Q, k);
+        a.Ag[hl + k - 1] = L::SQ2 * Xv.x;
+        a.Ax[hl + k - 1] = L::SQ2 * CUDART_PI * (double)k * Xv.y;
+      }
+    }
+    // FFT4: (Yy, 0) -> Ay, from registers into the buffer FFT3 no longer holds
+    cd* Y4 = (Z3 == A0) ? B0 : A0;
+    first_fwd(x4, Y4);
+    __syncthreads();
+    cd* Z4 = fft_lines_reg_passes<LG, false, 1, P>(Y4, Z3, tr, lane);
+    if (live) {
+      for (int k = lane + 1; k <= L::M; k += L::TPL) {
+        const double2 Xv = anal_read(Z4, ph, L::Q, k);
+        a.Ay[hl + k - 1] = L::SQ2 * Xv.x;
+      }
+    }
+    double* red = stage;  // TL * TPL doubles
+    red[threadIdx.x] = live ? dsum : 0.0;
+    __syncthreads();
+    if (live && lane == 0) {
+      double s = 0.0;
+      for (int i = 0; i < L::TPL; ++i) s += red[line * L::TPL + i];
+      a.part[((size_t)b * L::Q + q2) * 4 + 0] = s;
+    }
+    if (bad != 0x7fffffff) atomicMin(a.bad + b, bad);
+    return;
+  }
   // grid values kept in registers between the synthesis and analysis FFTs
   constexpr int QPL = (L::Q + L::TPL - 1) / L::TPL;
   double gx[QPL], gy[QPL], uu[QPL];
@@ -755,6 +964,11 @@ struct Hist2DArgs {
 
 template <int NT, int EPT>
 __global__ void __launch_bounds__(NT) k2_far(Hist2DArgs h, int beta) {
+  // rows are consumed in chunks of CH with their weights staged in shared
+  // memory (the same for every thread), RF rows in flight per thread
+  constexpr int CH = 64, RF = 8;
+  __shared__ double ws[CH + HB];   // Toeplitz weights a_{R0+1+rr-j} of the chunk
+  __shared__ double wb[CH * HB];   // bracket weights b_{j+(R0+1+rr)/m} of the chunk
   const int b = blockIdx.y;
   const int n = h.n0 + b;
   const int e0 = blockIdx.x * NT * EPT;
@@ -778,39 +992,59 @@ __global__ void __launch_bounds__(NT) k2_far(Hist2DArgs h, int beta) {
       cb[rr][i] = 0.0;
     }
   }
-  for (int j0 = 1; j0 <= J; j0 += 4) {  // 4 rows in flight per thread
-    double v[4][EPT];
+  for (int j0 = 1; j0 <= J; j0 += CH) {
+    const int jn = min(CH, J - j0 + 1);
+    const int s0 = R0 + 1 - j0 - (jn - 1);
+    __syncthreads();
+    for (int u = threadIdx.x; u < jn - 1 + HB; u += NT) ws[u] = h.afine[s0 + u];
+    __syncthreads();
+    for (int t0 = 0; t0 < jn; t0 += RF) {
+      double v[RF][EPT];
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < RF; ++t)
 #pragma unroll
-      for (int i = 0; i < EPT; ++i) {
-        const int e = e0 + threadIdx.x + i * NT;
-        v[t][i] = (e < h.MM && j0 + t <= J) ? path[(size_t)(j0 + t) * MM + e] : 0.0;
-      }
+        for (int i = 0; i < EPT; ++i) {
+          const int e = e0 + threadIdx.x + i * NT;
+          v[t][i] = (e < h.MM && t0 + t < jn) ? path[(size_t)(j0 + t0 + t) * MM + e] : 0.0;
+        }
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      if (j0 + t > J) break;
+      for (int t = 0; t < RF; ++t) {
+        if (t0 + t >= jn) break;
 #pragma unroll
-      for (int rr = 0; rr < HB; ++rr) {
-        const double w = h.afine[R0 + 1 + rr - (j0 + t)];
+        for (int rr = 0; rr < HB; ++rr) {
+          const double w = ws[rr - (t0 + t) + jn - 1];
 #pragma unroll
-        for (int i = 0; i < EPT; ++i) acc[rr][i] = fma(w, v[t][i], acc[rr][i]);
+          for (int i = 0; i < EPT; ++i) acc[rr][i] = fma(w, v[t][i], acc[rr][i]);
+        }
       }
     }
   }
   // coarse bracket rows r = R0+1 .. R0+HB: -m^-a sum_{j<n} b_{j+r/m} (U_{n-j} - U_{n-j-1})
-  for (int j = 0; j < n; ++j) {
-    double inc[EPT];
+  for (int j0 = 0; j0 < n; j0 += CH) {
+    const int jn = min(CH, n - j0);
+    __syncthreads();
+    for (int u = threadIdx.x; u < jn * HB; u += NT)
+      wb[u] = h.bfrac[(size_t)(j0 + u / HB) * h.m + R0 + 1 + u % HB];
+    __syncthreads();
+    for (int t0 = 0; t0 < jn; t0 += RF) {
+      double v[RF + 1][EPT];  // rows n-j0-t0 .. n-j0-t0-RF
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int e = e0 + threadIdx.x + i * NT;
-      inc[i] = (e < h.MM) ? h.U[(size_t)(n - j) * MM + e] - h.U[(size_t)(n - j - 1) * MM + e] : 0.0;
-    }
+      for (int t = 0; t <= RF; ++t)
 #pragma unroll
-    for (int rr = 0; rr < HB; ++rr) {
-      const double w = h.bfrac[(size_t)j * h.m + R0 + 1 + rr];
+        for (int i = 0; i < EPT; ++i) {
+          const int e = e0 + threadIdx.x + i * NT;
+          v[t][i] = (e < h.MM && t0 + t <= jn) ? h.U[(size_t)(n - j0 - t0 - t) * MM + e] : 0.0;
+        }
 #pragma unroll
-      for (int i = 0; i < EPT; ++i) cb[rr][i] = fma(w, inc[i], cb[rr][i]);
+      for (int t = 0; t < RF; ++t) {
+        if (t0 + t >= jn) break;
+#pragma unroll
+        for (int rr = 0; rr < HB; ++rr) {
+          const double w = wb[(t0 + t) * HB + rr];
+#pragma unroll
+          for (int i = 0; i < EPT; ++i) cb[rr][i] = fma(w, v[t][i] - v[t + 1][i], cb[rr][i]);
+        }
+      }
     }
   }
   double* out = h.far + (size_t)b * 2 * HB * MM;
