@@ -94,7 +94,8 @@ struct pf_ctx {
 namespace {  // 2-D engine entry points (defined in pf_engine2d.inc)
 int e2_fine_sweep(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, int m, bool with_bracket,
                   double* d_all = nullptr);
-int e2_coarse_step(pf_ctx* c, const double* d_H, int n, double* d_out);
+int e2_coarse_step(pf_ctx* c, const double* d_H, int n, double* d_out, int guess = 0,
+                   const double* gold = nullptr, const double* ucur = nullptr);
 int e2_run_coarse(pf_ctx* c, double* d_traj);
 int e2_correct(pf_ctx* c, const double* ucur, const double* fold, const double* gold, double* gnew, double* unext,
                int k, double* diff);

@@ -1090,6 +1090,16 @@ __global__ void k2_coarse_hist(const double* H, int n, long MM, const double* bf
   }
 }
 
+// coarse-step PCG guess (as the 1-D coarse_apply): kind 1 -> 2 U_n - U_{n-1}
+// (run_coarse), kind 2 -> G_old[n] + (U_next[n] - U_cur[n]) (correction sweep)
+__global__ void k2_coarse_guess(const double* H, int n, long MM, int kind, const double* gold, const double* ucur,
+                                double* X0) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < (size_t)MM; e += (size_t)gridDim.x * blockDim.x) {
+    const double xp = H[(size_t)n * MM + e];
+    X0[e] = kind == 1 ? fma(2.0, xp, -H[(size_t)(n - 1) * MM + e]) : gold[(size_t)n * MM + e] + (xp - ucur[(size_t)n * MM + e]);
+  }
+}
+
 // U_next[n+1] = F_old[n] + (G_new[n] - G_old[n])
 __global__ void k2_correct_row(const double* fold, const double* gnew, const double* gold, double* unext, long MM) {
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < (size_t)MM; e += (size_t)gridDim.x * blockDim.x)
