@@ -82,6 +82,12 @@ struct pf_ctx {
   double guard = 0;
   bool parareal_ready = false;
   int frozen = 0;  // leading nodes the last correction left bitwise unchanged
+  // Warm start of the parareal fine sweeps (2-D): each slice's path of the
+  // previous sweep, double-buffered and indexed by slice, seeds the PCG guess
+  // of the same substep of the next sweep (see k2_prep).
+  DevBuf wpaths[2];
+  int warm_iter = 0;        // parareal fine sweeps since init
+  double warm_diff = 1.0;   // last correction's diff (picks the guess order)
   int pending_lo = -1, pending_bs = 0;  // last async fine launch, decoded by pf_dev_check
   int* d_sync = nullptr;                 // sweep progress / ready / abort flags
   int sync_cap = 0;
@@ -93,7 +99,7 @@ struct pf_ctx {
 
 namespace {  // 2-D engine entry points (defined in pf_engine2d.inc)
 int e2_fine_sweep(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, int m, bool with_bracket,
-                  double* d_all = nullptr);
+                  double* d_all = nullptr, bool warm = false);
 int e2_coarse_step(pf_ctx* c, const double* d_H, int n, double* d_out, int guess = 0,
                    const double* gold = nullptr, const double* ucur = nullptr);
 int e2_run_coarse(pf_ctx* c, double* d_traj);
@@ -213,7 +219,11 @@ int ensure_status(pf_ctx* c, int n) {
 // helper CTA per slice (far history on otherwise idle SMs); else inline.
 int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, Status* d_st, int m_override = 0,
                 int hps_req = 1) {
-  if (c->kind == PF_SPACE_SINE2D) return e2_fine_sweep(c, d_u, n_lo, bs, d_out, c->grid.m, true);
+  if (c->kind == PF_SPACE_SINE2D) {
+    // the parareal driver's own sweeps (states == U) warm-start from the previous sweep
+    const bool warm = c->parareal_ready && d_u == c->U.p && m_override == 0;
+    return e2_fine_sweep(c, d_u, n_lo, bs, d_out, c->grid.m, true, nullptr, warm);
+  }
   const int m = m_override > 0 ? m_override : c->grid.m;
   const int hps = std::max(1, hps_req);
   if (c->paths.ensure((size_t)bs * (m + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "paths");
@@ -566,7 +576,9 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
 void pf_destroy(pf_ctx* c) {
   if (!c) return;
   if (c->device >= 0) cudaSetDevice(c->device);
-  for (DevBuf* b : {&c->U, &c->Unext, &c->paths, &c->fold, &c->gold, &c->gnew, &c->io, &c->scalar, &c->scratch}) b->release();
+  for (DevBuf* b : {&c->U, &c->Unext, &c->paths, &c->fold, &c->gold, &c->gnew, &c->io, &c->scalar, &c->scratch,
+                    &c->wpaths[0], &c->wpaths[1]})
+    b->release();
   for (void* p : {(void*)c->d_bfine, (void*)c->d_afine, (void*)c->d_bfrac, (void*)c->d_ext0, (void*)c->d_nodes, (void*)c->d_d1, (void*)c->d_qw,
                   (void*)c->d_tw, (void*)c->d_ph, (void*)c->d_status, (void*)c->d_sync})
     if (p) cudaFree(p);
@@ -812,6 +824,8 @@ int pf_dev_parareal_init(pf_ctx* c, const double* u0) {
   c->guard = 1e12 * std::max(host_norm(c, u0), 1.0);  // parareal.py:98
   c->parareal_ready = true;
   c->frozen = 0;
+  c->warm_iter = 0;
+  c->warm_diff = 1.0;
   return 0;
 }
 
@@ -845,6 +859,7 @@ int pf_dev_parareal_correct(pf_ctx* c, const double* d_fold, int k, double* diff
     int rc2 = e2_correct(c, c->U.p, c->fold.p, c->gold.p, c->gnew.p, c->Unext.p, k, &h2);
     if (rc2) return rc2;
     if (diff) *diff = h2;
+    c->warm_diff = h2;
     std::swap(c->U, c->Unext);
     return 0;
   }
@@ -858,6 +873,7 @@ int pf_dev_parareal_correct(pf_ctx* c, const double* d_fold, int k, double* diff
   if (cudaEventElapsedTime(&ms, c->ev0, c->ev1) == cudaSuccess) c->stats.last_coarse_ms = ms;
   if (rc) return rc;
   if (diff) *diff = h[0];
+  c->warm_diff = h[0];
   c->frozen = std::min((int)h[1], c->grid.nt);
   std::swap(c->U, c->Unext);  // u_curr = u_next (parareal.py:133)
   return 0;

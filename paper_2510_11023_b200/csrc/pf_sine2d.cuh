@@ -960,6 +960,8 @@ struct Hist2DArgs {
   const double* U;       // coarse states (nt+1, MM)
   const double* paths;   // (B, m+1, MM)
   double* far;           // (B, 2, HB, MM): [b][0] far history, [b][1] bracket
+  const double* old;     // previous parareal sweep's paths of the same slices, or nullptr
+  int warm_order;        // order of the drift extrapolation in the warm guess
 };
 
 template <int NT, int EPT>
@@ -1074,9 +1076,22 @@ __global__ void k2_prep(Hist2DArgs h, int r, double* HIST, double* CON, double* 
     for (int j = J + 1; j < r; ++j) acc = fma(h.afine[r - j], path[(size_t)j * MM + e], acc);
     HIST[(size_t)b * MM + e] = acc;
     CON[(size_t)b * MM + e] = far[(size_t)(HB + rr) * MM + e];
-    const double* w = kExtrap[p];
-    double g = w[0] * path[(size_t)(r - 1) * MM + e];
-    for (int j = 1; j <= p; ++j) g = fma(w[j], path[(size_t)(r - 1 - j) * MM + e], g);
+    double g;
+    if (h.old) {
+      // warm guess: the previous sweep's state at this substep plus the
+      // extrapolated drift of this sweep from it, x0 = old_r + sum_j w_j (c_{r-1-j} - old_{r-1-j})
+      const double* op = h.old + (size_t)b * (h.m + 1) * MM;
+      const int q = r - 1 < h.warm_order ? r - 1 : h.warm_order;
+      const double* w = kExtrap[q];
+      double dlt = 0.0;
+      for (int j = 0; j <= q; ++j)
+        dlt = fma(w[j], path[(size_t)(r - 1 - j) * MM + e] - op[(size_t)(r - 1 - j) * MM + e], dlt);
+      g = op[(size_t)r * MM + e] + dlt;
+    } else {
+      const double* w = kExtrap[p];
+      g = w[0] * path[(size_t)(r - 1) * MM + e];
+      for (int j = 1; j <= p; ++j) g = fma(w[j], path[(size_t)(r - 1 - j) * MM + e], g);
+    }
     X0[(size_t)b * MM + e] = g;
   }
 }
