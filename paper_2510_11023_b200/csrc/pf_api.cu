@@ -22,6 +22,7 @@
 #include "pf_kernels.cuh"
 #include "pf_sine1d.cuh"
 #include "pf_sine2d.cuh"
+#include "pf_line16.cuh"
 
 using pf::cd;
 using pf::Status;

@@ -1,0 +1,439 @@
+// 2-D line engine for Q = 256 (config 4: 128^2 modes on a 256^2 grid) with
+// register-resident FFTs.
+//
+// The radix-4 Stockham line FFT of pf_sine2d.cuh moves every element through
+// shared memory once per pass (4 passes at Q = 256) with a CTA barrier
+// between passes, and the 2-D kernels are shared-memory bound.  Here a line
+// is 16 lanes of one half-warp and the length-256 DFT is 16 x 16:
+//
+//   X[k1 + 16 k2] = sum_n2 w256^(n2 k1) w16^(n2 k2) sum_n1 x[16 n1 + n2] w16^(n1 k1)
+//
+// lane n2 holds x[16 n1 + n2] (n1 = 0..15), does a 16-point DFT in registers,
+// multiplies by w256^(n2 k1), the half-warp transposes through shared memory
+// (swizzled, conflict-free, __syncwarp only), and lane k1 does the second
+// 16-point DFT: it ends holding X[k1 + 16 k2], k2 = 0..15 -- which is exactly
+// the input layout of the next transform, so the PCG matvec's
+// synthesis -> pointwise -> analysis chain never leaves registers.  One
+// shared-memory round trip per FFT instead of four, no CTA barriers inside.
+//
+// The transform pairs (DCT-III/II via one complex FFT, Makhoul reordering)
+// and the data layouts are those of pf_sine2d.cuh; only the FFT changes, so
+// results agree with the radix-4 engine to rounding (both are checked against
+// oracle.Sine2D).
+#pragma once
+#include "pf_sine2d.cuh"
+
+namespace pf {
+
+struct L16 {
+  static constexpr int LG = 8, Q = 256, M = 128, TL = 16, NT = 256;
+  static constexpr int LS = Q + 1;  // line stride in cd (odd: staged tile writes are conflict-free)
+  static constexpr int STP = TL + 1;  // stage row stride in doubles
+  static constexpr double SQ2 = 1.4142135623730951;
+  static size_t smem_bytes() {
+    const size_t lines = sizeof(cd) * TL * LS, stage = sizeof(double) * 2 * Q * STP;
+    return sizeof(cd) * (256 + Q) + (lines > stage ? lines : stage);
+  }
+};
+
+template <bool INV>
+__device__ __forceinline__ void dft4(cd& a0, cd& a1, cd& a2, cd& a3) {
+  const cd t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = csub(a1, a3);
+  const cd mi3 = {t3.y, -t3.x};  // -i t3
+  a0 = cadd(t0, t2);
+  a1 = INV ? csub(t1, mi3) : cadd(t1, mi3);
+  a2 = csub(t0, t2);
+  a3 = INV ? cadd(t1, mi3) : csub(t1, mi3);
+}
+
+// multiply by w16^m (forward w = exp(-2 pi i / 16); INV: conjugate), m in {1,2,3,4,6,9}
+template <bool INV, int MM>
+__device__ __forceinline__ cd w16mul(cd a) {
+  constexpr double C = 0.92387953251128674, S = 0.38268343236508978, R = 0.70710678118654752;
+  constexpr double wr = MM == 1 ? C : MM == 2 ? R : MM == 3 ? S : MM == 4 ? 0.0 : MM == 6 ? -R : -C;
+  constexpr double wi0 = MM == 1 ? -S : MM == 2 ? -R : MM == 3 ? -C : MM == 4 ? -1.0 : MM == 6 ? -R : S;
+  constexpr double wi = INV ? -wi0 : wi0;
+  if constexpr (MM == 4) {
+    return INV ? cd{-a.y, a.x} : cd{a.y, -a.x};
+  } else {
+    return {a.x * wr - a.y * wi, a.x * wi + a.y * wr};
+  }
+}
+
+// in-place 16-point DFT, natural order in and out: v[n] -> X[k] = sum_n v[n] w16^(nk)
+template <bool INV>
+__device__ __forceinline__ void dft16(cd (&v)[16]) {
+  // n = 4a + b, k = c + 4d: DFT4 over a for each b, twiddle w16^(bc), DFT4 over b for each c
+#pragma unroll
+  for (int b = 0; b < 4; ++b) dft4<INV>(v[b], v[4 + b], v[8 + b], v[12 + b]);  // v[4c + b] = y[b][c]
+  v[4 + 1] = w16mul<INV, 1>(v[4 + 1]);
+  v[4 + 2] = w16mul<INV, 2>(v[4 + 2]);
+  v[4 + 3] = w16mul<INV, 3>(v[4 + 3]);
+  v[8 + 1] = w16mul<INV, 2>(v[8 + 1]);
+  v[8 + 2] = w16mul<INV, 4>(v[8 + 2]);
+  v[8 + 3] = w16mul<INV, 6>(v[8 + 3]);
+  v[12 + 1] = w16mul<INV, 3>(v[12 + 1]);
+  v[12 + 2] = w16mul<INV, 6>(v[12 + 2]);
+  v[12 + 3] = w16mul<INV, 9>(v[12 + 3]);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) dft4<INV>(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);  // v[4c + d] = X[c + 4d]
+  // transpose 4x4 to natural order: X[c + 4d] sits at v[4c + d]
+  cd t;
+  t = v[1]; v[1] = v[4]; v[4] = t;
+  t = v[2]; v[2] = v[8]; v[8] = t;
+  t = v[3]; v[3] = v[12]; v[12] = t;
+  t = v[6]; v[6] = v[9]; v[9] = t;
+  t = v[7]; v[7] = v[13]; v[13] = t;
+  t = v[11]; v[11] = v[14]; v[14] = t;
+}
+
+// Length-256 DFT of one line by its 16 lanes.  Entry: v[n1] = x[16 n1 + l].
+// Exit: v[k2] = X[l + 16 k2].  `buf` (this line's 256 cd) is scratch for the
+// transpose; `T[k1 * 16 + n2]` = w256^(k1 n2) (forward).
+template <bool INV>
+__device__ __forceinline__ void fft256(cd (&v)[16], cd* buf, const cd* T, int l) {
+  dft16<INV>(v);  // v[k1] = Y_l[k1]
+#pragma unroll
+  for (int k1 = 1; k1 < 16; ++k1) {
+    cd w = T[k1 * 16 + l];
+    if (INV) w.y = -w.y;
+    v[k1] = cmul(v[k1], w);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) buf[k1 * 16 + (l ^ k1)] = v[k1];
+  __syncwarp();
+#pragma unroll
+  for (int n2 = 0; n2 < 16; ++n2) v[n2] = buf[l * 16 + (n2 ^ l)];
+  __syncwarp();
+  dft16<INV>(v);
+}
+
+// synth_write / anal_read of pf_sine2d.cuh on an unswizzled line
+__device__ __forceinline__ void synth_write_plain(cd* W, const cd* ph, int k, double av, double bv) {
+  constexpr int Q = L16::Q, M = L16::M;
+  if (k < M) {
+    const cd p = ph[k], pq = ph[Q - k];
+    const cd v1 = {p.y * av, -p.x * av};
+    const cd v2 = {p.x * bv, p.y * bv};
+    W[k] = {v1.x - v2.y, v1.y + v2.x};
+    const cd u1 = {pq.x * av, pq.y * av};
+    const cd u2 = {pq.y * bv, -pq.x * bv};
+    W[Q - k] = {u1.x - u2.y, u1.y + u2.x};
+  } else {
+    const cd p = ph[M];
+    const cd v1 = {p.x * av + p.y * av, p.y * av - p.x * av};
+    const cd v2 = {p.x * bv + p.y * bv, p.y * bv - p.x * bv};
+    W[M] = {v1.x - v2.y, v1.y + v2.x};
+  }
+}
+
+__device__ __forceinline__ double2 anal_read_plain(const cd* Z, const cd* ph, int Q, int k) {
+  const cd a = Z[k], b = Z[Q - k], c = ph[k], c2 = ph[Q - k];
+  const double Dx = a.x - b.x, Dy = a.y + b.y;
+  return make_double2(0.5 * (c2.x * (b.x + a.x) + c2.y * (b.y - a.y)), 0.5 * (c.x * Dy - c.y * Dx));
+}
+
+// grid point of FFT position j (Makhoul reordering, pf_sine2d.cuh)
+__device__ __forceinline__ int q_of_pos(int pos) { return pos < 128 ? 2 * pos : 2 * (255 - pos) + 1; }
+__device__ __forceinline__ int pos_of_q(int q) { return (q & 1) ? (255 - (q >> 1)) : (q >> 1); }
+
+__device__ __forceinline__ void l16_setup(char* smem, const Sine2DArgs& a, cd*& T, cd*& ph, cd*& lines) {
+  T = reinterpret_cast<cd*>(smem);
+  ph = T + 256;
+  lines = ph + L16::Q;
+  for (int j = threadIdx.x; j < 256; j += L16::NT) T[j] = a.tw16[j];
+  for (int j = threadIdx.x; j < L16::Q; j += L16::NT) ph[j] = a.ph[j];
+  __syncthreads();
+}
+
+// synthesis-pair input of one line (lane-strided modes), then the lane's FFT inputs
+__device__ __forceinline__ void l16_load(const cd* W, int l, cd (&v)[16]) {
+#pragma unroll
+  for (int n1 = 0; n1 < 16; ++n1) v[n1] = W[16 * n1 + l];
+}
+
+// ---------------------------------------------------------------------------
+// rows, synthesis (along y): lines k1 -> H[q2][k1] (same contract as k2_rows_syn)
+// ---------------------------------------------------------------------------
+template <bool SETUP>
+__global__ void __launch_bounds__(256) k2_rows_syn16(Sine2DArgs a) {
+  using L = L16;
+  extern __shared__ __align__(16) char smem[];
+  const int b = blockIdx.y;
+  if (!SETUP && a.sc[b * 16 + S_DONE] != 0.0) return;
+  cd *T, *ph, *lines;
+  l16_setup(smem, a, T, ph, lines);
+  const int line = threadIdx.x >> 4, l = threadIdx.x & 15;
+  const int k1b = blockIdx.x * L::TL;
+  const int k1 = k1b + line + 1;
+  cd* W = lines + line * L::LS;
+  const size_t row = (size_t)(k1 - 1) * L::M;
+  const size_t MM = (size_t)L::M * L::M;
+  const double beta = SETUP ? 0.0 : a.sc[b * 16 + S_BETA];
+  double* st_s = reinterpret_cast<double*>(lines);
+  double* st_c = st_s + L::Q * L::STP;
+  constexpr int NF = SETUP ? 2 : 1;
+  for (int f = 0; f < NF; ++f) {
+    if (l == 0) W[0] = {0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < L::M / 16; ++i) {
+      const int k = l + 1 + 16 * i;
+      double av, bv;
+      if (SETUP) {
+        const double x0 = a.X0[b * a.sX0 + row + k - 1];
+        if (f == 0) {
+          av = L::SQ2 * a.Cp[b * a.sCp + row + k - 1];
+          bv = L::SQ2 * CUDART_PI * (double)k * x0;
+        } else {
+          av = L::SQ2 * x0;
+          bv = 0.0;
+        }
+      } else {
+        double* pp = a.P + (size_t)b * MM + row + k - 1;
+        const double pn = fma(beta, *pp, a.Z[(size_t)b * MM + row + k - 1]);
+        *pp = pn;
+        av = L::SQ2 * pn;
+        bv = L::SQ2 * CUDART_PI * (double)k * pn;
+      }
+      synth_write_plain(W, ph, k, av, bv);
+    }
+    __syncwarp();
+    cd v[16];
+    l16_load(W, l, v);
+    __syncwarp();
+    fft256<true>(v, W, T, l);
+    __syncthreads();  // every line is done with its buffer: reuse the lines as the stage
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) {
+      const int q = q_of_pos(l + 16 * k2);
+      st_s[q * L::STP + line] = (q & 1) ? -0.5 * v[k2].x : 0.5 * v[k2].x;
+      st_c[q * L::STP + line] = 0.5 * v[k2].y;
+    }
+    __syncthreads();
+    double* d_s = SETUP ? (f == 0 ? a.Hu : a.Hs) : a.Hs;
+    double* d_c = SETUP ? (f == 0 ? a.Hc : nullptr) : a.Hc;
+    for (int e = threadIdx.x; e < L::TL * L::Q; e += L::NT) {
+      const int q2 = e / L::TL, ll = e % L::TL;
+      const size_t o = ((size_t)b * L::Q + q2) * L::M + k1b + ll;
+      d_s[o] = st_s[q2 * L::STP + ll];
+      if (d_c) d_c[o] = st_c[q2 * L::STP + ll];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// columns (along x) for lines q2 (same contract as k2_cols)
+// ---------------------------------------------------------------------------
+template <bool SETUP>
+__global__ void __launch_bounds__(256) k2_cols16(Sine2DArgs a) {
+  using L = L16;
+  extern __shared__ __align__(16) char smem[];
+  const int b = blockIdx.y;
+  if (!SETUP && a.sc[b * 16 + S_DONE] != 0.0) return;
+  cd *T, *ph, *lines;
+  l16_setup(smem, a, T, ph, lines);
+  const int line = threadIdx.x >> 4, l = threadIdx.x & 15;
+  const int q2 = blockIdx.x * L::TL + line;
+  cd* W = lines + line * L::LS;
+  const size_t hl = ((size_t)b * L::Q + q2) * L::M;
+  const size_t gl = ((size_t)b * L::Q + q2) * L::Q;
+  auto synth = [&](const double* A, const double* Bk) {
+    if (l == 0) W[0] = {0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < L::M / 16; ++i) {
+      const int k = l + 1 + 16 * i;
+      synth_write_plain(W, ph, k, L::SQ2 * A[hl + k - 1], Bk ? L::SQ2 * CUDART_PI * (double)k * Bk[hl + k - 1] : 0.0);
+    }
+    __syncwarp();
+  };
+  auto store_natural = [&](const cd (&v)[16]) {
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) W[l + 16 * k2] = v[k2];
+    __syncwarp();
+  };
+  if (!SETUP) {
+    synth(a.Hc, a.Hs);
+    cd v[16];
+    l16_load(W, l, v);
+    __syncwarp();
+    fft256<true>(v, W, T, l);
+    // pointwise: Z_pos = (0.5 d_q) W_pos (see k2_cols)
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) {
+      const double d = 0.5 * a.D[gl + q_of_pos(l + 16 * k2)];
+      v[k2] = {d * v[k2].x, d * v[k2].y};
+    }
+    fft256<false>(v, W, T, l);
+    store_natural(v);
+#pragma unroll
+    for (int i = 0; i < L::M / 16; ++i) {
+      const int k = l + 1 + 16 * i;
+      const double2 X = anal_read_plain(W, ph, L::Q, k);
+      a.Ay[hl + k - 1] = L::SQ2 * X.x;
+      a.Ax[hl + k - 1] = L::SQ2 * CUDART_PI * (double)k * X.y;
+    }
+    return;
+  }
+  // setup: FFT1 (Hu, pi k Hs) -> u, Gx; FFT2 (Hc) -> Gy; coefficients; FFT3 (g, Yx); FFT4 (Yy)
+  const double wq = 1.0 / ((double)L::Q * (double)L::Q);
+  const double t = (double)(a.n0 + b) * a.dTs + a.tr;
+  const double emt = a.fn.id == 1 ? exp(-t) : 0.0;
+  cd v1[16], v2[16];
+  synth(a.Hu, a.Hs);
+  l16_load(W, l, v1);
+  __syncwarp();
+  fft256<true>(v1, W, T, l);
+  synth(a.Hc, nullptr);
+  l16_load(W, l, v2);
+  __syncwarp();
+  fft256<true>(v2, W, T, l);
+  double dsum = 0.0;
+  int bad = 0x7fffffff;
+  const double y2 = a.xq[q2];
+#pragma unroll
+  for (int k2 = 0; k2 < 16; ++k2) {
+    const int q1 = q_of_pos(l + 16 * k2);
+    const double u = (q1 & 1) ? -0.5 * v1[k2].x : 0.5 * v1[k2].x;
+    const double gx = 0.5 * v1[k2].y;
+    const double gy = (q1 & 1) ? -0.5 * v2[k2].x : 0.5 * v2[k2].x;
+    const double x1 = a.xq[q1];
+    const double Dv = fn_D(a.fn, x1, y2, t, u);
+    if (!isfinite(Dv)) bad = min(bad, q2 * L::Q + q1);
+    const double d = wq * Dv;
+    const double g = wq * (a.fn.id == 4 ? fn_f(a.fn, make_double2(0.0, 0.0), emt, u) : fn_f(a.fn, fn_xtab(x1), emt, u));
+    a.D[gl + q1] = d;
+    dsum += d;
+    const double sp4 = d * gy;
+    v1[k2] = {(q1 & 1) ? -g : g, d * gx};
+    v2[k2] = {(q1 & 1) ? -sp4 : sp4, 0.0};
+  }
+  fft256<false>(v1, W, T, l);
+  store_natural(v1);
+#pragma unroll
+  for (int i = 0; i < L::M / 16; ++i) {
+    const int k = l + 1 + 16 * i;
+    const double2 X = anal_read_plain(W, ph, L::Q, k);
+    a.Ag[hl + k - 1] = L::SQ2 * X.x;
+    a.Ax[hl + k - 1] = L::SQ2 * CUDART_PI * (double)k * X.y;
+  }
+  __syncwarp();
+  fft256<false>(v2, W, T, l);
+  store_natural(v2);
+#pragma unroll
+  for (int i = 0; i < L::M / 16; ++i) {
+    const int k = l + 1 + 16 * i;
+    a.Ay[hl + k - 1] = L::SQ2 * anal_read_plain(W, ph, L::Q, k).x;
+  }
+  // line partial of dbar: fixed-order butterfly over the line's 16 lanes
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+  if (l == 0) a.part[((size_t)b * L::Q + q2) * 4 + 0] = dsum;
+  if (bad != 0x7fffffff) atomicMin(a.bad + b, bad);
+}
+
+// ---------------------------------------------------------------------------
+// rows, analysis (along y) for lines k1 (same contract as k2_rows_ana)
+// ---------------------------------------------------------------------------
+template <bool SETUP>
+__global__ void __launch_bounds__(256) k2_rows_ana16(Sine2DArgs a) {
+  using L = L16;
+  extern __shared__ __align__(16) char smem[];
+  const int b = blockIdx.y;
+  if (!SETUP && a.sc[b * 16 + S_DONE] != 0.0) return;
+  cd *T, *ph, *lines;
+  l16_setup(smem, a, T, ph, lines);
+  const int line = threadIdx.x >> 4, l = threadIdx.x & 15;
+  const int k1b = blockIdx.x * L::TL;
+  const int k1 = k1b + line + 1;
+  cd* W = lines + line * L::LS;
+  const size_t MM = (size_t)L::M * L::M;
+  const size_t row = (size_t)(k1 - 1) * L::M;
+  constexpr int MPL = L::M / 16;
+  double kv[MPL], fv[MPL];
+#pragma unroll
+  for (int i = 0; i < MPL; ++i) kv[i] = fv[i] = 0.0;
+  const int nf = SETUP ? 2 : 1;
+  for (int f = 0; f < nf; ++f) {
+    const double* s1 = SETUP ? (f == 0 ? a.Ag : a.Ax) : a.Ax;
+    const double* s2 = SETUP ? (f == 0 ? a.Ay : nullptr) : a.Ay;
+    for (int e = threadIdx.x; e < L::TL * L::Q; e += L::NT) {
+      const int q2 = e / L::TL, ll = e % L::TL;
+      const size_t o = ((size_t)b * L::Q + q2) * L::M + k1b + ll;
+      const double g = s1[o], y = s2 ? s2[o] : 0.0;
+      lines[ll * L::LS + pos_of_q(q2)] = {(q2 & 1) ? -g : g, y};
+    }
+    __syncthreads();
+    cd v[16];
+    l16_load(W, l, v);
+    __syncwarp();
+    fft256<false>(v, W, T, l);
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) W[l + 16 * k2] = v[k2];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < MPL; ++i) {
+      const int k2 = l + 1 + 16 * i;
+      const double2 X = anal_read_plain(W, ph, L::Q, k2);
+      if (SETUP && f == 0) {
+        fv[i] = L::SQ2 * X.x;
+        kv[i] = L::SQ2 * CUDART_PI * (double)k2 * X.y;
+      } else if (SETUP) {
+        kv[i] += L::SQ2 * X.x;
+      } else {
+        kv[i] = L::SQ2 * X.x + L::SQ2 * CUDART_PI * (double)k2 * X.y;
+      }
+    }
+    __syncthreads();
+  }
+  double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+  const double gam = a.gam;
+  if (SETUP) {
+    const double dbar = a.sc[b * 16 + S_DBAR];
+#pragma unroll
+    for (int i = 0; i < MPL; ++i) {
+      const int k2 = l + 1 + 16 * i;
+      const size_t e = row + k2 - 1;
+      const double hist = a.HIST[b * a.sH + e];
+      const double con = a.CON ? a.CON[b * a.sC + e] : 0.0;
+      const double rhs = __dadd_rn(__dadd_rn(hist, __dmul_rn(gam, fv[i])), con);
+      const double x0 = a.X0[b * a.sX0 + e];
+      const double r = rhs - (x0 + gam * kv[i]);
+      const double kk = (double)k1 * (double)k1 + (double)k2 * (double)k2;
+      const double pinv = 1.0 / (1.0 + gam * dbar * (CUDART_PI * CUDART_PI) * kk);
+      const double z = pinv * r;
+      a.X[b * a.sX + e] = x0;
+      a.R[b * MM + e] = r;
+      a.Z[b * MM + e] = z;
+      a.P[b * MM + e] = z;
+      a.PINV[b * MM + e] = pinv;
+      p0 = fma(rhs, rhs, p0);
+      p1 = fma(r, r, p1);
+      p2 = fma(r, z, p2);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < MPL; ++i) {
+      const int k2 = l + 1 + 16 * i;
+      const size_t e = row + k2 - 1;
+      const double p = a.P[b * MM + e];
+      const double qv = p + gam * kv[i];
+      a.QV[b * MM + e] = qv;
+      p0 = fma(p, qv, p0);
+    }
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+    p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+    p2 += __shfl_xor_sync(0xffffffffu, p2, o);
+  }
+  if (l == 0) {
+    double* pp = a.part + ((size_t)b * L::Q + (k1 - 1)) * 4;
+    pp[1] = p0;
+    pp[2] = p1;
+    pp[3] = p2;
+  }
+}
+
+}  // namespace pf

@@ -234,6 +234,7 @@ struct Sine2DArgs {
   Fn fn;
   int M, Q, B;              // modes per axis, grid per axis, systems in the batch
   const cd* twp;            // per-pass twiddles (length-Q FFT)
+  const cd* tw16;           // Q = 256 engine: w256^(k1 n2), [k1][n2] (pf_line16.cuh)
   const cd* ph;             // exp(i pi j / 2Q)
   const double* xq;         // midpoints (q+1/2)/Q
   // per-system times t_b = (n0 + b) * dTs + tr  (fine: dTs = dT, tr = (r-1) dt)
