@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(256) k2_rows_syn16(Sine2DArgs a) {
 // columns (along x) for lines q2 (same contract as k2_cols)
 // ---------------------------------------------------------------------------
 template <bool SETUP>
-__global__ void __launch_bounds__(256) k2_cols16(Sine2DArgs a) {
+__global__ void __launch_bounds__(256, 2) k2_cols16(Sine2DArgs a) {
   using L = L16;
   extern __shared__ __align__(16) char smem[];
   const int b = blockIdx.y;
@@ -253,6 +253,10 @@ __global__ void __launch_bounds__(256) k2_cols16(Sine2DArgs a) {
     __syncwarp();
   };
   if (!SETUP) {
+    // the coefficient loads are independent of the transform: issue them first
+    double dv[16];
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) dv[k2] = a.D[gl + q_of_pos(l + 16 * k2)];
     synth(a.Hc, a.Hs);
     cd v[16];
     l16_load(W, l, v);
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(256) k2_cols16(Sine2DArgs a) {
     // pointwise: Z_pos = (0.5 d_q) W_pos (see k2_cols)
 #pragma unroll
     for (int k2 = 0; k2 < 16; ++k2) {
-      const double d = 0.5 * a.D[gl + q_of_pos(l + 16 * k2)];
+      const double d = 0.5 * dv[k2];
       v[k2] = {d * v[k2].x, d * v[k2].y};
     }
     fft256<false>(v, W, T, l);
