@@ -175,23 +175,35 @@ __global__ void __launch_bounds__(256) k2_rows_syn16(Sine2DArgs a) {
   constexpr int NF = SETUP ? 2 : 1;
   for (int f = 0; f < NF; ++f) {
     if (l == 0) W[0] = {0.0, 0.0};
+    // loads first (the P stores below would otherwise order them one by one)
+    constexpr int MPL = L::M / 16;
+    double ld1[MPL], ld2[MPL];
 #pragma unroll
-    for (int i = 0; i < L::M / 16; ++i) {
+    for (int i = 0; i < MPL; ++i) {
+      const size_t e = row + l + 16 * i;
+      if (SETUP) {
+        ld1[i] = a.X0[b * a.sX0 + e];
+        ld2[i] = f == 0 ? a.Cp[b * a.sCp + e] : 0.0;
+      } else {
+        ld1[i] = a.P[(size_t)b * MM + e];
+        ld2[i] = a.Z[(size_t)b * MM + e];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MPL; ++i) {
       const int k = l + 1 + 16 * i;
       double av, bv;
       if (SETUP) {
-        const double x0 = a.X0[b * a.sX0 + row + k - 1];
         if (f == 0) {
-          av = L::SQ2 * a.Cp[b * a.sCp + row + k - 1];
-          bv = L::SQ2 * CUDART_PI * (double)k * x0;
+          av = L::SQ2 * ld2[i];
+          bv = L::SQ2 * CUDART_PI * (double)k * ld1[i];
         } else {
-          av = L::SQ2 * x0;
+          av = L::SQ2 * ld1[i];
           bv = 0.0;
         }
       } else {
-        double* pp = a.P + (size_t)b * MM + row + k - 1;
-        const double pn = fma(beta, *pp, a.Z[(size_t)b * MM + row + k - 1]);
-        *pp = pn;
+        const double pn = fma(beta, ld1[i], ld2[i]);
+        a.P[(size_t)b * MM + row + k - 1] = pn;
         av = L::SQ2 * pn;
         bv = L::SQ2 * CUDART_PI * (double)k * pn;
       }
@@ -240,10 +252,16 @@ __global__ void __launch_bounds__(256, 2) k2_cols16(Sine2DArgs a) {
   const size_t gl = ((size_t)b * L::Q + q2) * L::Q;
   auto synth = [&](const double* A, const double* Bk) {
     if (l == 0) W[0] = {0.0, 0.0};
+    double av[L::M / 16], bv[L::M / 16];
+#pragma unroll
+    for (int i = 0; i < L::M / 16; ++i) {
+      av[i] = A[hl + l + 16 * i];
+      bv[i] = Bk ? Bk[hl + l + 16 * i] : 0.0;
+    }
 #pragma unroll
     for (int i = 0; i < L::M / 16; ++i) {
       const int k = l + 1 + 16 * i;
-      synth_write_plain(W, ph, k, L::SQ2 * A[hl + k - 1], Bk ? L::SQ2 * CUDART_PI * (double)k * Bk[hl + k - 1] : 0.0);
+      synth_write_plain(W, ph, k, L::SQ2 * av[i], L::SQ2 * CUDART_PI * (double)k * bv[i]);
     }
     __syncwarp();
   };
@@ -361,11 +379,21 @@ __global__ void __launch_bounds__(256) k2_rows_ana16(Sine2DArgs a) {
   for (int f = 0; f < nf; ++f) {
     const double* s1 = SETUP ? (f == 0 ? a.Ag : a.Ax) : a.Ax;
     const double* s2 = SETUP ? (f == 0 ? a.Ay : nullptr) : a.Ay;
-    for (int e = threadIdx.x; e < L::TL * L::Q; e += L::NT) {
+    // all 16 tile loads of a thread in flight at once, then the staging stores
+    constexpr int NE = L::TL * L::Q / L::NT;
+    double gv[NE], yv[NE];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      const int e = threadIdx.x + i * L::NT;
+      const size_t o = ((size_t)b * L::Q + e / L::TL) * L::M + k1b + e % L::TL;
+      gv[i] = s1[o];
+      yv[i] = s2 ? s2[o] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      const int e = threadIdx.x + i * L::NT;
       const int q2 = e / L::TL, ll = e % L::TL;
-      const size_t o = ((size_t)b * L::Q + q2) * L::M + k1b + ll;
-      const double g = s1[o], y = s2 ? s2[o] : 0.0;
-      lines[ll * L::LS + pos_of_q(q2)] = {(q2 & 1) ? -g : g, y};
+      lines[ll * L::LS + pos_of_q(q2)] = {(q2 & 1) ? -gv[i] : gv[i], yv[i]};
     }
     __syncthreads();
     cd v[16];
@@ -394,14 +422,22 @@ __global__ void __launch_bounds__(256) k2_rows_ana16(Sine2DArgs a) {
   const double gam = a.gam;
   if (SETUP) {
     const double dbar = a.sc[b * 16 + S_DBAR];
+    double hv[MPL], cv[MPL], xv[MPL];
+#pragma unroll
+    for (int i = 0; i < MPL; ++i) {
+      const size_t e = row + l + 16 * i;
+      hv[i] = a.HIST[b * a.sH + e];
+      cv[i] = a.CON ? a.CON[b * a.sC + e] : 0.0;
+      xv[i] = a.X0[b * a.sX0 + e];
+    }
 #pragma unroll
     for (int i = 0; i < MPL; ++i) {
       const int k2 = l + 1 + 16 * i;
       const size_t e = row + k2 - 1;
-      const double hist = a.HIST[b * a.sH + e];
-      const double con = a.CON ? a.CON[b * a.sC + e] : 0.0;
+      const double hist = hv[i];
+      const double con = cv[i];
       const double rhs = __dadd_rn(__dadd_rn(hist, __dmul_rn(gam, fv[i])), con);
-      const double x0 = a.X0[b * a.sX0 + e];
+      const double x0 = xv[i];
       const double r = rhs - (x0 + gam * kv[i]);
       const double kk = (double)k1 * (double)k1 + (double)k2 * (double)k2;
       const double pinv = 1.0 / (1.0 + gam * dbar * (CUDART_PI * CUDART_PI) * kk);
@@ -416,11 +452,14 @@ __global__ void __launch_bounds__(256) k2_rows_ana16(Sine2DArgs a) {
       p2 = fma(r, z, p2);
     }
   } else {
+    double pv[MPL];
+#pragma unroll
+    for (int i = 0; i < MPL; ++i) pv[i] = a.P[b * MM + row + l + 16 * i];
 #pragma unroll
     for (int i = 0; i < MPL; ++i) {
       const int k2 = l + 1 + 16 * i;
       const size_t e = row + k2 - 1;
-      const double p = a.P[b * MM + e];
+      const double p = pv[i];
       const double qv = p + gam * kv[i];
       a.QV[b * MM + e] = qv;
       p0 = fma(p, qv, p0);
