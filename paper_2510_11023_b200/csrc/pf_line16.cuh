@@ -234,6 +234,37 @@ __global__ void __launch_bounds__(256) k2_rows_syn16(Sine2DArgs a) {
   }
 }
 
+// setup pointwise of one column line at the lane's 16 grid points: u, Gx from
+// the first synthesis FFT (v1), Gy from the second (v2) -> D on the grid, the
+// inputs of the analysis FFTs (v1 <- (g, d Gx), x4 <- d Gy), dbar partial
+template <int FID>
+__device__ __forceinline__ void l16_pointwise(const Sine2DArgs& a, int q2, double t, double emt, size_t gl,
+                                              cd (&v1)[16], const cd (&v2)[16], double (&x4)[16], double& dsum,
+                                              int& bad) {
+  const double wq = 1.0 / ((double)L16::Q * (double)L16::Q);
+  const int l = threadIdx.x & 15;
+  Fn f1 = a.fn;
+  if (FID != 0) f1.id = FID;  // constant-folds the functor switches
+  const double y2 = a.xq[q2];
+#pragma unroll
+  for (int k2 = 0; k2 < 16; ++k2) {
+    const int q1 = q_of_pos(l + 16 * k2);
+    const double u = (q1 & 1) ? -0.5 * v1[k2].x : 0.5 * v1[k2].x;
+    const double gx = 0.5 * v1[k2].y;
+    const double gy = (q1 & 1) ? -0.5 * v2[k2].x : 0.5 * v2[k2].x;
+    const double x1 = a.xq[q1];
+    const double Dv = fn_D(f1, x1, y2, t, u);
+    if (!isfinite(Dv)) bad = min(bad, q2 * L16::Q + q1);
+    const double d = wq * Dv;
+    const double g = wq * (f1.id == 4 ? fn_f(f1, make_double2(0.0, 0.0), emt, u) : fn_f(f1, fn_xtab(x1), emt, u));
+    a.D[gl + q1] = d;
+    dsum += d;
+    const double sp4 = d * gy;
+    v1[k2] = {(q1 & 1) ? -g : g, d * gx};
+    x4[k2] = (q1 & 1) ? -sp4 : sp4;  // FFT4 input is real
+  }
+}
+
 // ---------------------------------------------------------------------------
 // columns (along x) for lines q2 (same contract as k2_cols)
 // ---------------------------------------------------------------------------
@@ -312,23 +343,14 @@ __global__ void __launch_bounds__(256, 2) k2_cols16(Sine2DArgs a) {
   fft256<true>(v2, W, T, l);
   double dsum = 0.0;
   int bad = 0x7fffffff;
-  const double y2 = a.xq[q2];
-#pragma unroll
-  for (int k2 = 0; k2 < 16; ++k2) {
-    const int q1 = q_of_pos(l + 16 * k2);
-    const double u = (q1 & 1) ? -0.5 * v1[k2].x : 0.5 * v1[k2].x;
-    const double gx = 0.5 * v1[k2].y;
-    const double gy = (q1 & 1) ? -0.5 * v2[k2].x : 0.5 * v2[k2].x;
-    const double x1 = a.xq[q1];
-    const double Dv = fn_D(a.fn, x1, y2, t, u);
-    if (!isfinite(Dv)) bad = min(bad, q2 * L::Q + q1);
-    const double d = wq * Dv;
-    const double g = wq * (a.fn.id == 4 ? fn_f(a.fn, make_double2(0.0, 0.0), emt, u) : fn_f(a.fn, fn_xtab(x1), emt, u));
-    a.D[gl + q1] = d;
-    dsum += d;
-    const double sp4 = d * gy;
-    v1[k2] = {(q1 & 1) ? -g : g, d * gx};
-    v2[k2] = {(q1 & 1) ? -sp4 : sp4, 0.0};
+  double x4[16];
+  // one functor switch outside the point loop: each functor's loop is straight-line code
+  switch (a.fn.id) {
+    case 1: l16_pointwise<1>(a, q2, t, emt, gl, v1, v2, x4, dsum, bad); break;
+    case 2: l16_pointwise<2>(a, q2, t, emt, gl, v1, v2, x4, dsum, bad); break;
+    case 3: l16_pointwise<3>(a, q2, t, emt, gl, v1, v2, x4, dsum, bad); break;
+    case 4: l16_pointwise<4>(a, q2, t, emt, gl, v1, v2, x4, dsum, bad); break;
+    default: l16_pointwise<0>(a, q2, t, emt, gl, v1, v2, x4, dsum, bad); break;
   }
   fft256<false>(v1, W, T, l);
   store_natural(v1);
@@ -340,6 +362,8 @@ __global__ void __launch_bounds__(256, 2) k2_cols16(Sine2DArgs a) {
     a.Ax[hl + k - 1] = L::SQ2 * CUDART_PI * (double)k * X.y;
   }
   __syncwarp();
+#pragma unroll
+  for (int k2 = 0; k2 < 16; ++k2) v2[k2] = {x4[k2], 0.0};
   fft256<false>(v2, W, T, l);
   store_natural(v2);
 #pragma unroll
