@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(256) k2_rows_syn16(Sine2DArgs a) {
   const size_t row = (size_t)(k1 - 1) * L::M;
   const size_t MM = (size_t)L::M * L::M;
   const double beta = SETUP ? 0.0 : a.sc[b * 16 + S_BETA];
+  const double dbar = a.sc[b * 16 + S_DBAR];
   double* st_s = reinterpret_cast<double*>(lines);
   double* st_c = st_s + L::Q * L::STP;
   constexpr int NF = SETUP ? 2 : 1;
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(256) k2_rows_syn16(Sine2DArgs a) {
         ld2[i] = f == 0 ? a.Cp[b * a.sCp + e] : 0.0;
       } else {
         ld1[i] = a.P[(size_t)b * MM + e];
-        ld2[i] = a.Z[(size_t)b * MM + e];
+        ld2[i] = a.R[(size_t)b * MM + e];
       }
     }
 #pragma unroll
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(256) k2_rows_syn16(Sine2DArgs a) {
           bv = 0.0;
         }
       } else {
-        const double pn = fma(beta, ld1[i], ld2[i]);
+        const double pn = fma(beta, ld1[i], pinv2d(a.gam, dbar, k1, k) * ld2[i]);  // p = z + beta p
         a.P[(size_t)b * MM + row + k - 1] = pn;
         av = L::SQ2 * pn;
         bv = L::SQ2 * CUDART_PI * (double)k * pn;
@@ -463,14 +464,10 @@ __global__ void __launch_bounds__(256) k2_rows_ana16(Sine2DArgs a) {
       const double rhs = __dadd_rn(__dadd_rn(hist, __dmul_rn(gam, fv[i])), con);
       const double x0 = xv[i];
       const double r = rhs - (x0 + gam * kv[i]);
-      const double kk = (double)k1 * (double)k1 + (double)k2 * (double)k2;
-      const double pinv = 1.0 / (1.0 + gam * dbar * (CUDART_PI * CUDART_PI) * kk);
-      const double z = pinv * r;
+      const double z = pinv2d(gam, dbar, k1, k2) * r;
       a.X[b * a.sX + e] = x0;
       a.R[b * MM + e] = r;
-      a.Z[b * MM + e] = z;
       a.P[b * MM + e] = z;
-      a.PINV[b * MM + e] = pinv;
       p0 = fma(rhs, rhs, p0);
       p1 = fma(r, r, p1);
       p2 = fma(r, z, p2);

@@ -246,7 +246,7 @@ struct Sine2DArgs {
   const double* HIST; long sH;  // L1 history term
   const double* CON; long sC;   // coarse bracket (nullptr: zero)
   double* X; long sX;           // solution (written in place)
-  double *R, *Z, *P, *QV, *PINV;  // (B, M*M) work
+  double *R, *P, *QV;  // (B, M*M) work (z = pinv r is recomputed, never stored)
   // line arrays (B, Q, M): y-transformed, x-modes
   double *Hu, *Hs, *Hc, *Ag, *Ax, *Ay;
   double* D;                    // (B, Q, Q) W*d on the grid [q2][q1]
@@ -254,6 +254,13 @@ struct Sine2DArgs {
   double* sc;                   // (B, 16) per-system scalars
   int* bad;                     // (B) smallest non-finite grid index (INT_MAX none)
 };
+
+// Jacobi-like preconditioner 1/(1 + gam dbar pi^2 (k1^2 + k2^2)),
+// recomputed where needed (explicit roundings: every kernel gets the same bits)
+__device__ __forceinline__ double pinv2d(double gam, double dbar, int k1, int k2) {
+  const double kk = __dadd_rn(__dmul_rn((double)k1, (double)k1), __dmul_rn((double)k2, (double)k2));
+  return __ddiv_rn(1.0, __dadd_rn(1.0, __dmul_rn(__dmul_rn(__dmul_rn(gam, dbar), CUDART_PI * CUDART_PI), kk)));
+}
 
 // per-system scalar slots
 enum { S_DBAR = 0, S_BB, S_RR, S_RZ, S_PQ, S_ALPHA, S_BETA, S_THR, S_DONE, S_ZERO, S_IT, S_FAIL };
@@ -351,7 +358,8 @@ __global__ void __launch_bounds__(256) k2_rows_syn(Sine2DArgs a) {
           }
         } else {
           double* pp = a.P + (size_t)b * L::M * L::M + row + k - 1;
-          const double pn = fma(beta, *pp, a.Z[(size_t)b * L::M * L::M + row + k - 1]);
+          const double z = pinv2d(a.gam, a.sc[b * 16 + S_DBAR], k1, k) * a.R[(size_t)b * L::M * L::M + row + k - 1];
+          const double pn = fma(beta, *pp, z);
           *pp = pn;
           av = L::SQ2 * pn;
           bv = L::SQ2 * CUDART_PI * (double)k * pn;
@@ -789,14 +797,10 @@ __global__ void __launch_bounds__(256) k2_rows_ana(Sine2DArgs a) {
           const double rhs = __dadd_rn(__dadd_rn(hist, __dmul_rn(gam, fv[i])), con);
           const double x0 = a.X0[b * a.sX0 + e];
           const double r = rhs - (x0 + gam * kv[i]);
-          const double kk = (double)k1 * (double)k1 + (double)k2 * (double)k2;
-          const double pinv = 1.0 / (1.0 + gam * dbar * (CUDART_PI * CUDART_PI) * kk);
-          const double z = pinv * r;
+          const double z = pinv2d(gam, dbar, k1, k2) * r;
           a.X[b * a.sX + e] = x0;
           a.R[b * MM + e] = r;
-          a.Z[b * MM + e] = z;
           a.P[b * MM + e] = z;
-          a.PINV[b * MM + e] = pinv;
           p0 = fma(rhs, rhs, p0);
           p1 = fma(r, r, p1);
           p2 = fma(r, z, p2);
@@ -843,6 +847,7 @@ __global__ void __launch_bounds__(256) k2_update(Sine2DArgs a) {
   const int b = blockIdx.y;
   if (a.sc[b * 16 + S_DONE] != 0.0) return;
   const double alpha = a.sc[b * 16 + S_ALPHA];
+  const double dbar = a.sc[b * 16 + S_DBAR];
   const size_t MM = (size_t)L::M * L::M;
   __shared__ double red[2 * 256];
   // one CTA per (k1 tile of 256/M... ) : threads over modes of TLU rows
@@ -855,9 +860,8 @@ __global__ void __launch_bounds__(256) k2_update(Sine2DArgs a) {
       double* x = a.X + b * a.sX + e;
       *x = fma(alpha, a.P[b * MM + e], *x);
       const double r = fma(-alpha, a.QV[b * MM + e], a.R[b * MM + e]);
-      const double z = a.PINV[b * MM + e] * r;
+      const double z = pinv2d(a.gam, dbar, k1 + 1, k2 + 1) * r;
       a.R[b * MM + e] = r;
-      a.Z[b * MM + e] = z;
       rr = fma(r, r, rr);
       rz = fma(r, z, rz);
     }
