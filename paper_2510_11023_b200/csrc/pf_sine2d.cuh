@@ -1077,17 +1077,10 @@ __global__ void k2_prep(Hist2DArgs h, int r, double* HIST, double* CON, double* 
   const double* path = h.paths + (size_t)b * (h.m + 1) * MM;
   const double* far = h.far + (size_t)b * 2 * HB * MM;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < MM; e += (size_t)gridDim.x * blockDim.x) {
-    // the (< 2 HB) near rows, all loads in flight at once; v[q-1] = row r-q
-    double v[2 * HB - 1];
-#pragma unroll
-    for (int q = 1; q < 2 * HB; ++q) v[q - 1] = (r - q > J) ? path[(size_t)(r - q) * MM + e] : 0.0;
     double acc = far[(size_t)rr * MM + e];
-    const double con = far[(size_t)(HB + rr) * MM + e];
-#pragma unroll
-    for (int q = 2 * HB - 1; q >= 1; --q)  // j = r - q ascending, as the reference's einsum order
-      if (r - q > J) acc = fma(h.afine[q], v[q - 1], acc);
+    for (int j = J + 1; j < r; ++j) acc = fma(h.afine[r - j], path[(size_t)j * MM + e], acc);
     HIST[(size_t)b * MM + e] = acc;
-    CON[(size_t)b * MM + e] = con;
+    CON[(size_t)b * MM + e] = far[(size_t)(HB + rr) * MM + e];
     double g;
     if (h.old) {
       // warm guess: the previous sweep's state at this substep plus the
