@@ -188,8 +188,8 @@ pf::Cheb1DParams cheb_params(const pf_ctx* c) {
       constexpr int NT = 32, EPT = 1; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
     case V_S6: { using SP = pf::Sine1D<32, 1, 6>; using SPP = pf::Sine1DParams; \
       constexpr int NT = 32, EPT = 1; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
-    case V_S7: { using SP = pf::Sine1D<32, 2, 7>; using SPP = pf::Sine1DParams; \
-      constexpr int NT = 32, EPT = 2; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
+    case V_S7: { using SP = pf::Sine1D<128, 1, 7>; using SPP = pf::Sine1DParams; \
+      constexpr int NT = 128, EPT = 1; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
     case V_S8: { using SP = pf::Sine1D<64, 2, 8>; using SPP = pf::Sine1DParams; \
       constexpr int NT = 64, EPT = 2; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
     case V_S9: { using SP = pf::Sine1D<128, 2, 9>; using SPP = pf::Sine1DParams; \
