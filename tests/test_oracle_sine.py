@@ -107,3 +107,17 @@ def test_sine2d_parareal_finite_termination():
     sp = oracle.Sine2D(4)
     g = oracle.TimeGrids(1.0, 4, 4)
     assert oracle.exactness_check(prob, sp, g, 4) <= 1e-10
+
+
+def test_full_size_config3_oracle_fixture_contract():
+    """tests/golden/oracle_cfg3_full.npz (make_oracle_full.py: the oracle at the
+    full config-3 size, ~2 h of CPU) -- the fixture the device is held to in
+    test_gpu_parity.py::test_config3_full_size_properties."""
+    import os
+
+    f = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "oracle_cfg3_full.npz"))
+    assert f["states"].shape == (65, 512) and f["fine_endpoints"].shape == (64, 512)
+    assert int(f["iterations"]) == 7 == len(f["diffs"])
+    d = f["diffs"]
+    assert np.all(d[1:] < d[:-1]) and d[-1] < 1e-12 <= d[-2]
+    assert np.isfinite(f["states"]).all()
