@@ -23,6 +23,7 @@
 #include "pf_sine1d.cuh"
 #include "pf_sine2d.cuh"
 #include "pf_line16.cuh"
+#include "pf_line32.cuh"
 
 using pf::cd;
 using pf::Status;
