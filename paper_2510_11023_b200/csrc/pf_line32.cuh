@@ -204,7 +204,7 @@ __device__ __forceinline__ void l32_pointwise(const Sine2DArgs& a, int q2, doubl
     const double gy = (q1 & 1) ? -0.5 * v2[k2].x : 0.5 * v2[k2].x;
     const double x1 = a.xq[q1];
     const double Dv = fn_D(f1, x1, y2, t, u);
-    if (!isfinite(Dv)) bad = min(bad, q2 * L32::Q + q1);
+    if (!isfinite(Dv)) bad = min(bad, q1 * L32::Q + q2);  // oracle.Sine2D flat index [x1][x2]
     const double d = wq * Dv;
     const double g = wq * (f1.id == 4 ? fn_f(f1, make_double2(0.0, 0.0), emt, u) : fn_f(f1, fn_xtab(x1), emt, u));
     a.D[gl + q1] = d;

@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(256) k2_cols(Sine2DArgs a) {
       if (live) {
         const double x1 = a.xq[q1];
         const double Dv = fn_D(a.fn, x1, a.xq[q2], t, u);
-        if (!isfinite(Dv)) bad = min(bad, q2 * L::Q + q1);
+        if (!isfinite(Dv)) bad = min(bad, q1 * L::Q + q2);  // oracle.Sine2D flat index [x1][x2]
         const double d = wq * Dv;
         const double g = wq * (a.fn.id == 4 ? fn_f(a.fn, make_double2(0.0, 0.0), emt, u)
                                             : fn_f(a.fn, fn_xtab(x1), emt, u));
@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(256) k2_cols(Sine2DArgs a) {
             if (f == 0) {
               const double x1 = a.xq[q1];
               const double Dv = fn_D(a.fn, x1, a.xq[q2], t, uu[i]);
-              if (!isfinite(Dv)) bad = min(bad, q2 * L::Q + q1);
+              if (!isfinite(Dv)) bad = min(bad, q1 * L::Q + q2);  // oracle.Sine2D flat index [x1][x2]
               d = wq * Dv;
               g = wq * (a.fn.id == 4 ? fn_f(a.fn, make_double2(0.0, 0.0), emt, uu[i])
                                      : fn_f(a.fn, fn_xtab(x1), emt, uu[i]));
