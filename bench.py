@@ -233,6 +233,8 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parareal", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the torch.distributed (NCCL) driver even at one rank (exercises the multi-GPU path)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -246,7 +248,7 @@ def main():
     import torch.distributed as dist
 
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2510_11023_b200 as pfb
@@ -346,12 +348,28 @@ def main():
            "api": "paper_2510_11023_b200.fine_sweep_intervals (ctypes -> pf_fine_sweep)"}
 
     parareal = None
-    if not args.no_parareal and world == 1 and dims == 1:
+    if not args.no_parareal and not dist.is_initialized():
         t0 = time.perf_counter()
         it, rep = pfb.parareal_solve(prob, op, grids, tol=cfg["tol"], k_max=P + 1)
         parareal = {"time_to_tol_s": time.perf_counter() - t0, "iterations": rep.iterations,
                     "stop_reason": rep.stop_reason, "final_diff": rep.diffs[-1],
                     "note": "public API parareal_solve, initial coarse sweep + all iterations"}
+    elif not args.no_parareal:
+        # multi-GPU time-to-tol: slices sharded over the ranks, one NCCL all-gather
+        # of the fine endpoints per iteration, replicated correction (parallel.py)
+        from paper_2510_11023_b200.parallel import DeviceOps, DistributedParareal
+        dp = DistributedParareal(DeviceOps(prob, op, grids, local), P)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = dp.solve(tol=cfg["tol"], k_max=P + 1)
+        torch.cuda.synchronize()
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        parareal = {"time_to_tol_s": float(t.item()), "iterations": res["k"], "stop_reason": res["stop_reason"],
+                    "final_diff": res["diffs"][-1],
+                    "note": f"parallel.DistributedParareal over {world} ranks (NCCL all-gather of F_old per "
+                            "iteration), initial coarse sweep + all iterations, max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -368,7 +386,7 @@ def main():
             "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "parareal": parareal,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

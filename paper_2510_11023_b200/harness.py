@@ -1,0 +1,133 @@
+"""Fine-versus-parareal timing on the device path.
+
+Mirrors the benchmark half of ``parafrac/harness.py`` (``bench_point`` /
+``bench_sweep``, ``harness.py:85-123``): at ``dof = nt * m`` fine steps it
+times the full-history serial solver (``run_fine_sequential``) against
+``parareal_solve`` -- here both through the sm_100a library -- and records the
+speedup, the iteration count and the last increment.  Timing keeps the
+reference's convention (minimum over ``reps`` after ``warmup`` discarded
+runs, ``time.perf_counter``, ``harness.py:65-73``); the allocation columns are
+host-side ``tracemalloc`` peaks of a separate pass, as there (device memory is
+owned by the library and not traced).
+
+The truncation study of ``harness.py:126-227`` is scalar analysis of the L1
+operator, not on the solver path, and is not part of the device build.
+"""
+
+from __future__ import annotations
+
+import time
+import tracemalloc
+from dataclasses import dataclass
+
+from .l1 import TimeGrids
+from .problems import CONFIGS, get_problem
+from .solver import parareal_solve, run_fine_sequential
+from .spaces import build_operator, build_sine_operator
+
+__all__ = ["BenchRecord", "bench_point", "bench_sweep", "make_operator"]
+
+
+@dataclass(frozen=True)
+class BenchRecord:
+    """One sweep point; the field set of ``harness.py:46-60`` (CSV columns of ``cli bench``)."""
+
+    dof: int
+    nt: int
+    m: int
+    degree: int
+    threads: int
+    wall_fine: float
+    wall_parareal: float
+    speedup: float
+    iterations: int
+    final_diff: float
+    peak_alloc_fine: int
+    peak_alloc_parareal: int
+
+
+def make_operator(problem, degree=None, space=None, dims=None):
+    """Spatial operator for a CLI/harness run.
+
+    ``space`` "chebyshev" is the reference's collocation operator
+    (``build_operator(degree, a, b)``, ``spectral.py:74``); "sine" the
+    sine-Galerkin space with ``degree`` modes per axis.  Left as ``None`` it is
+    "sine" for the BASELINE problems ``cfg1``..``cfg5`` (their modes and
+    dimension from ``CONFIGS`` unless ``degree`` / ``dims`` override them) and
+    "chebyshev" otherwise, the reference's default.
+    """
+    name = getattr(problem, "name", "")
+    cfg = None
+    if name.startswith("cfg") and name[3:].isdigit():
+        cfg = CONFIGS.get(int(name[3:]))
+    if space is None:
+        space = "sine" if cfg is not None else "chebyshev"
+    if space == "chebyshev":
+        return build_operator(16 if degree is None else int(degree), problem.a, problem.b)
+    if space == "sine":
+        modes = degree if degree is not None else (cfg["modes"] if cfg is not None else 16)
+        d = dims if dims is not None else (cfg["dims"] if cfg is not None else 1)
+        return build_sine_operator(int(modes), dims=int(d))
+    raise ValueError(f"unknown space {space!r}; choices: chebyshev, sine")
+
+
+def _min_time(fn, reps, warmup):
+    result = None
+    for _ in range(warmup):
+        result = fn()
+    best = float("inf")
+    for _ in range(max(1, reps)):
+        t0 = time.perf_counter()
+        result = fn()
+        best = min(best, time.perf_counter() - t0)
+    return best, result
+
+
+def _host_peak(fn):
+    tracemalloc.start()
+    try:
+        fn()
+        return int(tracemalloc.get_traced_memory()[1])
+    finally:
+        tracemalloc.stop()
+
+
+def bench_point(problem_name, dof, *, alpha=None, degree=16, m=32, tol=1e-10, k_max=20, threads=1,
+                reps=3, warmup=1, measure_memory=True, space=None, dims=None):
+    """Serial fine solver vs parareal at ``nt * m ~= dof`` fine steps (``harness.py:85-117``).
+
+    ``m`` is clipped to ``[1, dof]`` and ``nt = dof // m``; the realised dof
+    is recorded.  ``threads`` is recorded and otherwise ignored (the device
+    batches every slice).
+    """
+    if dof < 1:
+        raise ValueError("dof must be a positive integer")
+    m_eff = max(1, min(int(m), int(dof)))
+    nt = max(1, int(dof) // m_eff)
+    problem = get_problem(problem_name, alpha=alpha)
+    op = make_operator(problem, degree, space, dims)
+    grids = TimeGrids(problem.t_final, nt, m_eff)
+
+    def fine():
+        return run_fine_sequential(problem, op, grids)
+
+    def para():
+        return parareal_solve(problem, op, grids, tol=tol, k_max=k_max, threads=threads)
+
+    t_fine, _ = _min_time(fine, reps, warmup)
+    t_para, (_, report) = _min_time(para, reps, warmup)
+    return BenchRecord(
+        dof=nt * m_eff, nt=nt, m=m_eff,
+        degree=int(getattr(op, "degree", getattr(op, "modes", 0))),
+        threads=int(threads), wall_fine=t_fine, wall_parareal=t_para, speedup=t_fine / t_para,
+        iterations=report.iterations, final_diff=report.diffs[-1],
+        peak_alloc_fine=_host_peak(fine) if measure_memory else 0,
+        peak_alloc_parareal=_host_peak(para) if measure_memory else 0,
+    )
+
+
+def bench_sweep(problem_name, dofs, **kwargs):
+    """``bench_point`` over every dof of the sweep, in order (``harness.py:120-123``)."""
+    if not dofs:
+        raise ValueError("benchmark sweep must not be empty")
+    return [bench_point(problem_name, d, **kwargs) for d in dofs]

@@ -119,7 +119,7 @@ class DistributedParareal:
         send = self.ops.empty(self.chunk)
         if hi > lo:
             send[: hi - lo].copy_(local[: hi - lo])
-        if self.world == 1:
+        if not self.dist.is_initialized():
             return send[: hi - lo]
         recv = self.ops.empty(self.chunk * self.world)
         self.dist.all_gather_into_tensor(recv, send, group=self.group)
