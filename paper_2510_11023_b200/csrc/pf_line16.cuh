@@ -153,6 +153,79 @@ __device__ __forceinline__ void l16_load(const cd* W, int l, cd (&v)[16]) {
 }
 
 // ---------------------------------------------------------------------------
+// Shuffle-based synthesis input and analysis output (no shared-memory round
+// trip).  Lane l of a line owns the modes k = l + 16 i (l >= 1, i = 0..7) or
+// k = 16 i (lane 0, i = 1..8) -- a partition of 1..M.  The fft256 input slot
+// j = 16 n1 + l carries mode j (j < M) or mode Q - j (j > M); the output Z[k]
+// sits in lane k % 16, register k / 16.  So slot n1 < 8 of lane l is its own
+// mode i = n1, slot n1 >= 8 is own mode 15 - n1 of lane 16 - l (lane 0: its
+// own mode 16 - n1), and the analysis partner Z[Q - k] of own mode i is
+// register 15 - i of lane 16 - l (lane 0: its own register 16 - i).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int l16_own_mode(int i, int l) {
+  return l == 0 ? 16 * i : (i < 8 ? l + 16 * i : 0);  // 0: no mode in this slot
+}
+
+__device__ __forceinline__ int l16_partner(int l) { return ((int)threadIdx.x & 16) | ((16 - l) & 15); }
+
+// slot j != 0 of a synthesis pair from its mode's (av, bv) (synth_write_plain per slot; ph[j] is
+// the phase of slot j in both halves)
+__device__ __forceinline__ cd l16_slot(int j, cd p, double av, double bv) {
+  if (j < L16::M) {
+    const cd v1 = {p.y * av, -p.x * av}, v2 = {p.x * bv, p.y * bv};
+    return {v1.x - v2.y, v1.y + v2.x};
+  }
+  if (j == L16::M) {
+    const cd v1 = {p.x * av + p.y * av, p.y * av - p.x * av}, v2 = {p.x * bv + p.y * bv, p.y * bv - p.x * bv};
+    return {v1.x - v2.y, v1.y + v2.x};
+  }
+  const cd u1 = {p.x * av, p.y * av}, u2 = {p.y * bv, -p.x * bv};
+  return {u1.x - u2.y, u1.y + u2.x};
+}
+
+// fft256 input v[n1] = W[16 n1 + l] of a synthesis pair from the lane's own (av, bv)
+__device__ __forceinline__ void l16_synth_own(const double (&av)[9], const double (&bv)[9], const cd* ph, int l,
+                                              cd (&v)[16]) {
+  const int src = l16_partner(l);
+#pragma unroll
+  for (int n1 = 0; n1 < 16; ++n1) {
+    const int j = 16 * n1 + l;
+    double A, B;
+    if (n1 < 8) {
+      A = av[n1];
+      B = bv[n1];
+    } else {
+      const double pa = __shfl_sync(0xffffffffu, av[15 - n1], src);
+      const double pb = __shfl_sync(0xffffffffu, bv[15 - n1], src);
+      A = l == 0 ? av[16 - n1] : pa;
+      B = l == 0 ? bv[16 - n1] : pb;
+    }
+    v[n1] = j == 0 ? cd{0.0, 0.0} : l16_slot(j, ph[j], A, B);
+  }
+}
+
+// analysis pair of the lane's own modes from the fft256 output v[i] = Z[l + 16 i]:
+// emit(i, k, X1, X2) with X1 the sine (S^T) and X2 the cosine (S'^T / (sqrt2 pi k)) part
+template <class F>
+__device__ __forceinline__ void l16_anal_own(const cd (&v)[16], const cd* ph, int l, F&& emit) {
+  const int src = l16_partner(l);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    cd b = {0.0, 0.0};
+    if (i < 8) {
+      b.x = __shfl_sync(0xffffffffu, v[15 - i].x, src);
+      b.y = __shfl_sync(0xffffffffu, v[15 - i].y, src);
+    }
+    const int k = l16_own_mode(i, l);
+    if (k == 0) continue;
+    if (l == 0) b = v[16 - i];
+    const cd a = v[i], c = ph[k], c2 = ph[L16::Q - k];
+    const double Dx = a.x - b.x, Dy = a.y + b.y;
+    emit(i, k, 0.5 * (c2.x * (b.x + a.x) + c2.y * (b.y - a.y)), 0.5 * (c.x * Dy - c.y * Dx));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // rows, synthesis (along y): lines k1 -> H[q2][k1] (same contract as k2_rows_syn)
 // ---------------------------------------------------------------------------
 template <bool SETUP>
@@ -175,45 +248,44 @@ __global__ void __launch_bounds__(256) k2_rows_syn16(Sine2DArgs a) {
   double* st_c = st_s + L::Q * L::STP;
   constexpr int NF = SETUP ? 2 : 1;
   for (int f = 0; f < NF; ++f) {
-    if (l == 0) W[0] = {0.0, 0.0};
-    // loads first (the P stores below would otherwise order them one by one)
-    constexpr int MPL = L::M / 16;
-    double ld1[MPL], ld2[MPL];
+    // own-mode loads first (the P stores below would otherwise order them one by one)
+    double ld1[9], ld2[9], av[9], bv[9];
 #pragma unroll
-    for (int i = 0; i < MPL; ++i) {
-      const size_t e = row + l + 16 * i;
-      if (SETUP) {
-        ld1[i] = a.X0[b * a.sX0 + e];
-        ld2[i] = f == 0 ? a.Cp[b * a.sCp + e] : 0.0;
-      } else {
-        ld1[i] = a.P[(size_t)b * MM + e];
-        ld2[i] = a.R[(size_t)b * MM + e];
+    for (int i = 0; i < 9; ++i) {
+      const int k = l16_own_mode(i, l);
+      ld1[i] = ld2[i] = 0.0;
+      if (k > 0) {
+        const size_t e = row + k - 1;
+        if (SETUP) {
+          ld1[i] = a.X0[b * a.sX0 + e];
+          ld2[i] = f == 0 ? a.Cp[b * a.sCp + e] : 0.0;
+        } else {
+          ld1[i] = a.P[(size_t)b * MM + e];
+          ld2[i] = a.R[(size_t)b * MM + e];
+        }
       }
     }
 #pragma unroll
-    for (int i = 0; i < MPL; ++i) {
-      const int k = l + 1 + 16 * i;
-      double av, bv;
+    for (int i = 0; i < 9; ++i) {
+      const int k = l16_own_mode(i, l);
+      av[i] = bv[i] = 0.0;
+      if (k == 0) continue;
       if (SETUP) {
         if (f == 0) {
-          av = L::SQ2 * ld2[i];
-          bv = L::SQ2 * CUDART_PI * (double)k * ld1[i];
+          av[i] = L::SQ2 * ld2[i];
+          bv[i] = L::SQ2 * CUDART_PI * (double)k * ld1[i];
         } else {
-          av = L::SQ2 * ld1[i];
-          bv = 0.0;
+          av[i] = L::SQ2 * ld1[i];
         }
       } else {
         const double pn = fma(beta, ld1[i], pinv2d(a.gam, dbar, k1, k) * ld2[i]);  // p = z + beta p
         a.P[(size_t)b * MM + row + k - 1] = pn;
-        av = L::SQ2 * pn;
-        bv = L::SQ2 * CUDART_PI * (double)k * pn;
+        av[i] = L::SQ2 * pn;
+        bv[i] = L::SQ2 * CUDART_PI * (double)k * pn;
       }
-      synth_write_plain(W, ph, k, av, bv);
     }
-    __syncwarp();
     cd v[16];
-    l16_load(W, l, v);
-    __syncwarp();
+    l16_synth_own(av, bv, ph, l, v);
     fft256<true>(v, W, T, l);
     __syncthreads();  // every line is done with its buffer: reuse the lines as the stage
 #pragma unroll
@@ -282,35 +354,30 @@ __global__ void __launch_bounds__(256, 2) k2_cols16(Sine2DArgs a) {
   cd* W = lines + line * L::LS;
   const size_t hl = ((size_t)b * L::Q + q2) * L::M;
   const size_t gl = ((size_t)b * L::Q + q2) * L::Q;
-  auto synth = [&](const double* A, const double* Bk) {
-    if (l == 0) W[0] = {0.0, 0.0};
-    double av[L::M / 16], bv[L::M / 16];
+  // synthesis pair (A, pi k Bk) of the line's modes -> fft256 input v
+  auto synth = [&](const double* A, const double* Bk, cd (&v)[16]) {
+    double av[9], bv[9];
 #pragma unroll
-    for (int i = 0; i < L::M / 16; ++i) {
-      av[i] = A[hl + l + 16 * i];
-      bv[i] = Bk ? Bk[hl + l + 16 * i] : 0.0;
+    for (int i = 0; i < 9; ++i) {
+      const int k = l16_own_mode(i, l);
+      av[i] = k > 0 ? A[hl + k - 1] : 0.0;
+      bv[i] = (k > 0 && Bk) ? Bk[hl + k - 1] : 0.0;
     }
 #pragma unroll
-    for (int i = 0; i < L::M / 16; ++i) {
-      const int k = l + 1 + 16 * i;
-      synth_write_plain(W, ph, k, L::SQ2 * av[i], L::SQ2 * CUDART_PI * (double)k * bv[i]);
+    for (int i = 0; i < 9; ++i) {
+      const int k = l16_own_mode(i, l);
+      av[i] = L::SQ2 * av[i];
+      bv[i] = L::SQ2 * CUDART_PI * (double)k * bv[i];
     }
-    __syncwarp();
-  };
-  auto store_natural = [&](const cd (&v)[16]) {
-#pragma unroll
-    for (int k2 = 0; k2 < 16; ++k2) W[l + 16 * k2] = v[k2];
-    __syncwarp();
+    l16_synth_own(av, bv, ph, l, v);
   };
   if (!SETUP) {
     // the coefficient loads are independent of the transform: issue them first
     double dv[16];
 #pragma unroll
     for (int k2 = 0; k2 < 16; ++k2) dv[k2] = a.D[gl + q_of_pos(l + 16 * k2)];
-    synth(a.Hc, a.Hs);
     cd v[16];
-    l16_load(W, l, v);
-    __syncwarp();
+    synth(a.Hc, a.Hs, v);
     fft256<true>(v, W, T, l);
     // pointwise: Z_pos = (0.5 d_q) W_pos (see k2_cols)
 #pragma unroll
@@ -319,14 +386,10 @@ __global__ void __launch_bounds__(256, 2) k2_cols16(Sine2DArgs a) {
       v[k2] = {d * v[k2].x, d * v[k2].y};
     }
     fft256<false>(v, W, T, l);
-    store_natural(v);
-#pragma unroll
-    for (int i = 0; i < L::M / 16; ++i) {
-      const int k = l + 1 + 16 * i;
-      const double2 X = anal_read_plain(W, ph, L::Q, k);
-      a.Ay[hl + k - 1] = L::SQ2 * X.x;
-      a.Ax[hl + k - 1] = L::SQ2 * CUDART_PI * (double)k * X.y;
-    }
+    l16_anal_own(v, ph, l, [&](int, int k, double X1, double X2) {
+      a.Ay[hl + k - 1] = L::SQ2 * X1;
+      a.Ax[hl + k - 1] = L::SQ2 * CUDART_PI * (double)k * X2;
+    });
     return;
   }
   // setup: FFT1 (Hu, pi k Hs) -> u, Gx; FFT2 (Hc) -> Gy; coefficients; FFT3 (g, Yx); FFT4 (Yy)
@@ -334,13 +397,9 @@ __global__ void __launch_bounds__(256, 2) k2_cols16(Sine2DArgs a) {
   const double t = (double)(a.n0 + b) * a.dTs + a.tr;
   const double emt = a.fn.id == 1 ? exp(-t) : 0.0;
   cd v1[16], v2[16];
-  synth(a.Hu, a.Hs);
-  l16_load(W, l, v1);
-  __syncwarp();
+  synth(a.Hu, a.Hs, v1);
   fft256<true>(v1, W, T, l);
-  synth(a.Hc, nullptr);
-  l16_load(W, l, v2);
-  __syncwarp();
+  synth(a.Hc, nullptr, v2);
   fft256<true>(v2, W, T, l);
   double dsum = 0.0;
   int bad = 0x7fffffff;
@@ -354,24 +413,14 @@ __global__ void __launch_bounds__(256, 2) k2_cols16(Sine2DArgs a) {
     default: l16_pointwise<0>(a, q2, t, emt, gl, v1, v2, x4, dsum, bad); break;
   }
   fft256<false>(v1, W, T, l);
-  store_natural(v1);
-#pragma unroll
-  for (int i = 0; i < L::M / 16; ++i) {
-    const int k = l + 1 + 16 * i;
-    const double2 X = anal_read_plain(W, ph, L::Q, k);
-    a.Ag[hl + k - 1] = L::SQ2 * X.x;
-    a.Ax[hl + k - 1] = L::SQ2 * CUDART_PI * (double)k * X.y;
-  }
-  __syncwarp();
+  l16_anal_own(v1, ph, l, [&](int, int k, double X1, double X2) {
+    a.Ag[hl + k - 1] = L::SQ2 * X1;
+    a.Ax[hl + k - 1] = L::SQ2 * CUDART_PI * (double)k * X2;
+  });
 #pragma unroll
   for (int k2 = 0; k2 < 16; ++k2) v2[k2] = {x4[k2], 0.0};
   fft256<false>(v2, W, T, l);
-  store_natural(v2);
-#pragma unroll
-  for (int i = 0; i < L::M / 16; ++i) {
-    const int k = l + 1 + 16 * i;
-    a.Ay[hl + k - 1] = L::SQ2 * anal_read_plain(W, ph, L::Q, k).x;
-  }
+  l16_anal_own(v2, ph, l, [&](int, int k, double X1, double) { a.Ay[hl + k - 1] = L::SQ2 * X1; });
   // line partial of dbar: fixed-order butterfly over the line's 16 lanes
 #pragma unroll
   for (int o = 8; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
@@ -396,7 +445,7 @@ __global__ void __launch_bounds__(256) k2_rows_ana16(Sine2DArgs a) {
   cd* W = lines + line * L::LS;
   const size_t MM = (size_t)L::M * L::M;
   const size_t row = (size_t)(k1 - 1) * L::M;
-  constexpr int MPL = L::M / 16;
+  constexpr int MPL = 9;  // own modes l16_own_mode(i, l)
   double kv[MPL], fv[MPL];
 #pragma unroll
   for (int i = 0; i < MPL; ++i) kv[i] = fv[i] = 0.0;
@@ -425,22 +474,16 @@ __global__ void __launch_bounds__(256) k2_rows_ana16(Sine2DArgs a) {
     l16_load(W, l, v);
     __syncwarp();
     fft256<false>(v, W, T, l);
-#pragma unroll
-    for (int k2 = 0; k2 < 16; ++k2) W[l + 16 * k2] = v[k2];
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < MPL; ++i) {
-      const int k2 = l + 1 + 16 * i;
-      const double2 X = anal_read_plain(W, ph, L::Q, k2);
+    l16_anal_own(v, ph, l, [&](int i, int k2, double X1, double X2) {
       if (SETUP && f == 0) {
-        fv[i] = L::SQ2 * X.x;
-        kv[i] = L::SQ2 * CUDART_PI * (double)k2 * X.y;
+        fv[i] = L::SQ2 * X1;
+        kv[i] = L::SQ2 * CUDART_PI * (double)k2 * X2;
       } else if (SETUP) {
-        kv[i] += L::SQ2 * X.x;
+        kv[i] += L::SQ2 * X1;
       } else {
-        kv[i] = L::SQ2 * X.x + L::SQ2 * CUDART_PI * (double)k2 * X.y;
+        kv[i] = L::SQ2 * X1 + L::SQ2 * CUDART_PI * (double)k2 * X2;
       }
-    }
+    });
     __syncthreads();
   }
   double p0 = 0.0, p1 = 0.0, p2 = 0.0;
@@ -450,14 +493,16 @@ __global__ void __launch_bounds__(256) k2_rows_ana16(Sine2DArgs a) {
     double hv[MPL], cv[MPL], xv[MPL];
 #pragma unroll
     for (int i = 0; i < MPL; ++i) {
-      const size_t e = row + l + 16 * i;
-      hv[i] = a.HIST[b * a.sH + e];
-      cv[i] = a.CON ? a.CON[b * a.sC + e] : 0.0;
-      xv[i] = a.X0[b * a.sX0 + e];
+      const int k2 = l16_own_mode(i, l);
+      const size_t e = row + (k2 > 0 ? k2 - 1 : 0);
+      hv[i] = k2 > 0 ? a.HIST[b * a.sH + e] : 0.0;
+      cv[i] = (k2 > 0 && a.CON) ? a.CON[b * a.sC + e] : 0.0;
+      xv[i] = k2 > 0 ? a.X0[b * a.sX0 + e] : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < MPL; ++i) {
-      const int k2 = l + 1 + 16 * i;
+      const int k2 = l16_own_mode(i, l);
+      if (k2 == 0) continue;
       const size_t e = row + k2 - 1;
       const double hist = hv[i];
       const double con = cv[i];
@@ -475,10 +520,14 @@ __global__ void __launch_bounds__(256) k2_rows_ana16(Sine2DArgs a) {
   } else {
     double pv[MPL];
 #pragma unroll
-    for (int i = 0; i < MPL; ++i) pv[i] = a.P[b * MM + row + l + 16 * i];
+    for (int i = 0; i < MPL; ++i) {
+      const int k2 = l16_own_mode(i, l);
+      pv[i] = k2 > 0 ? a.P[b * MM + row + k2 - 1] : 0.0;
+    }
 #pragma unroll
     for (int i = 0; i < MPL; ++i) {
-      const int k2 = l + 1 + 16 * i;
+      const int k2 = l16_own_mode(i, l);
+      if (k2 == 0) continue;
       const size_t e = row + k2 - 1;
       const double p = pv[i];
       const double qv = p + gam * kv[i];
