@@ -437,6 +437,7 @@ __global__ void __launch_bounds__(256, 2) k2_rows_ana32(Sine2DArgs a) {
     pp[2] = p1;
     pp[3] = p2;
   }
+  if (!SETUP && pcg_is_last_cta(a, b)) pcg_alpha(a, b);
 }
 
 }  // namespace pf

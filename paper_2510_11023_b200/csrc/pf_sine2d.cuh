@@ -253,6 +253,9 @@ struct Sine2DArgs {
   double* part;                 // (B, Q, 4) per-line partial sums
   double* sc;                   // (B, 16) per-system scalars
   int* bad;                     // (B) smallest non-finite grid index (INT_MAX none)
+  int* tickets;                 // (B) CTA arrivals of the fused PCG tail (zero between launches)
+  int* remaining;               // unfinished systems after the current PCG iteration
+  int maxit;                    // PCG iteration cap
 };
 
 // Jacobi-like preconditioner 1/(1 + gam dbar pi^2 (k1^2 + k2^2)),
@@ -264,6 +267,79 @@ __device__ __forceinline__ double pinv2d(double gam, double dbar, int k1, int k2
 
 // per-system scalar slots
 enum { S_DBAR = 0, S_BB, S_RR, S_RZ, S_PQ, S_ALPHA, S_BETA, S_THR, S_DONE, S_ZERO, S_IT, S_FAIL };
+
+// ---------------------------------------------------------------------------
+// PCG scalar reductions fused into the launches that produce their partials.
+// Every CTA of system b takes a ticket after storing its partials; the last
+// CTA of the system to arrive sums the M line partials in the fixed order of
+// k2_reduce (so the result is bitwise that of the separate reduce launch).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool pcg_is_last_cta(const Sine2DArgs& a, int b) {
+  __shared__ int s_last;
+  __threadfence();  // this CTA's QV rows and partials before its ticket
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int t = atomicAdd(a.tickets + b, 1);
+    s_last = (t == (int)gridDim.x - 1);
+    if (s_last) a.tickets[b] = 0;  // every CTA of b has arrived: reset for the next launch
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  return true;
+}
+
+// last CTA of a PCG row-analysis launch: alpha = rz / pq, pq from the M line
+// partials in the fixed order of k2_reduce kind 1
+__device__ __forceinline__ void pcg_alpha(const Sine2DArgs& a, int b) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  double s = 0.0;
+  for (int k = lane; k < a.M; k += 32) s += __ldcg(a.part + ((size_t)b * a.Q + k) * 4 + 1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane != 0) return;
+  double* sc = a.sc + b * 16;
+  const double alpha = sc[S_RZ] / s;
+  sc[S_ALPHA] = alpha;
+  if (!isfinite(alpha)) {
+    sc[S_FAIL] = 1.0;
+    sc[S_DONE] = 1.0;
+  }
+}
+
+// last CTA of a PCG update launch: (rr, rz) from the M row partials in the fixed
+// order of k2_reduce kind 2, convergence / beta, the unfinished count
+__device__ __forceinline__ void pcg_converge(const Sine2DArgs& a, int b) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  double s0 = 0.0, s1 = 0.0;
+  for (int k = lane; k < a.M; k += 32) {
+    s0 += __ldcg(a.part + ((size_t)b * a.Q + k) * 4 + 2);
+    s1 += __ldcg(a.part + ((size_t)b * a.Q + k) * 4 + 3);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  if (lane != 0) return;
+  double* sc = a.sc + b * 16;
+  sc[S_IT] += 1.0;
+  if (!isfinite(s0)) {
+    sc[S_FAIL] = 1.0;
+    sc[S_DONE] = 1.0;
+  } else if (!(s0 > sc[S_THR])) {
+    sc[S_DONE] = 1.0;
+  } else if (sc[S_IT] >= (double)a.maxit) {
+    sc[S_FAIL] = 2.0;
+    sc[S_DONE] = 1.0;
+  } else {
+    sc[S_BETA] = s1 / sc[S_RZ];
+    sc[S_RZ] = s1;
+  }
+  if (sc[S_DONE] == 0.0) atomicAdd(a.remaining, 1);
+}
 
 template <int LG>
 struct Line2D {
@@ -838,6 +914,7 @@ __global__ void __launch_bounds__(256) k2_rows_ana(Sine2DArgs a) {
     pp[2] = s1;
     pp[3] = s2;
   }
+  if (!SETUP && pcg_is_last_cta(a, b)) pcg_alpha(a, b);
 }
 
 // CG vector update over modes: x += alpha p, r -= alpha q, z = pinv r; line partials (rr, rz)
@@ -881,6 +958,7 @@ __global__ void __launch_bounds__(256) k2_update(Sine2DArgs a) {
     pp[2] = s0;
     pp[3] = s1;
   }
+  if (pcg_is_last_cta(a, b)) pcg_converge(a, b);
 }
 
 // Per-system scalar reductions: one warp per system sums the M line
