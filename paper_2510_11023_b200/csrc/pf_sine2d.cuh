@@ -1021,6 +1021,24 @@ __global__ void k2_reduce(Sine2DArgs a, int kind, int maxit, int* remaining) {
   if (sc[S_DONE] == 0.0) atomicAdd(remaining, 1);
 }
 
+// end of a sweep substep r: per-system PCG iteration count and first failure
+// (the sweep reads both once at its end instead of once per substep)
+// `flag` (the PCG unfinished counter, free between substeps) is set to 1 when
+// any system has failed so far, 0 otherwise, for the host's early exit.
+__global__ void k2_record(Sine2DArgs a, int r, int4* ff, double* it_acc, int* flag) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;  // *flag is 0 here: every PCG system has finished
+  if (b >= a.B) return;
+  const double* sc = a.sc + b * 16;
+  it_acc[b] += sc[S_IT];
+  if (ff[b].x == 0) {
+    if (a.bad[b] < 0x7f7f7f7f)
+      ff[b] = make_int4(r, 1, a.bad[b], 0);
+    else if (sc[S_FAIL] != 0.0)
+      ff[b] = make_int4(r, 2, (int)sc[S_FAIL], 0);
+  }
+  if (ff[b].x != 0) atomicOr(flag, 1);
+}
+
 // zero right-hand side: the solution is zero (stepping's solve of (I+gam K) x = 0)
 __global__ void k2_zero_fix(Sine2DArgs a) {
   const int b = blockIdx.y;
