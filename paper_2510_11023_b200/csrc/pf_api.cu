@@ -74,7 +74,7 @@ struct pf_ctx {
   cd *d_tw = nullptr, *d_ph = nullptr;  // d_tw: per-pass twiddle tables
   long len_fine = 0, len_frac = 0;
   // work buffers
-  DevBuf U, Unext, paths, fold, gold, gnew, io, scalar, scratch;
+  DevBuf U, Unext, paths, fold, gold, gnew, io, scalar, scratch, brk;
   Status* d_status = nullptr;
   int status_cap = 0;
   std::vector<Status> h_status;
@@ -245,6 +245,15 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   cm.m = m;
   double* dp = c->paths.p;
   PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+  cm.brk = nullptr;
+  if (n_lo + bs > 1) {  // some slice has a coarse history: its bracket rows, one batched GEMM
+    if (c->brk.ensure((size_t)bs * m * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "bracket");
+    constexpr int RT = 16;
+    const dim3 gb((unsigned)((c->size + 255) / 256), (unsigned)((m + RT - 1) / RT), (unsigned)bs);
+    pf::k_bracket_all<RT><<<gb, 256, 0, c->stream>>>(cm, d_u, n_lo, c->brk.p);
+    c->stats.kernel_launches += 1;
+    cm.brk = c->brk.p;
+  }
   PF_DISPATCH(c, {
     auto kern = pf::k_fine_sweep<SP, SPP, NT, EPT>;
     int per_sm = 0;
@@ -407,6 +416,17 @@ int pf_debug_phases(long long* out16, int reset) {
   return PF_OK;
 }
 
+// Entry and exit times (globaltimer ns) of each slice CTA of the last decoded
+// 1-D fine sweep: out[2 i] = entry, out[2 i + 1] = exit.
+int pf_debug_slice_times_ns(const pf_ctx* c, long long* out, int n) {
+  if (!c || !out || n < 0 || n > (int)c->h_status.size()) return PF_ERR_ARGUMENT;
+  for (int i = 0; i < n; ++i) {
+    out[2 * i] = c->h_status[i].t_start;
+    out[2 * i + 1] = c->h_status[i].t_end;
+  }
+  return PF_OK;
+}
+
 int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* space, const pf_weights* weights,
               int device, pf_ctx** out) {
   if (!out) return PF_ERR_ARGUMENT;
@@ -514,19 +534,34 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
   PF_CUDA(c, cudaMemcpy(c->d_afine, h_afine.data(), sizeof(double) * h_afine.size(), cudaMemcpyHostToDevice));
   PF_CUDA(c, cudaMemcpy(c->d_bfrac, c->h_bfrac.data(), sizeof(double) * need_frac, cudaMemcpyHostToDevice));
   if (c->kind == PF_SPACE_SINE1D && alpha < 1.0) {
-    // slice-0 guess weights: Lagrange extrapolation to tau(r) from tau(r-1..r-1-p), tau(k) = (k dt)^alpha
+    // PCG guess weights of the fine substeps (global index k = n m + r, local
+    // r = 1..m): Lagrange extrapolation in tau = t^alpha from the slice's rows
+    // r-1 .. r-1-p, tau(k) = (k dt)^alpha.  The order p follows the t^alpha
+    // layer (tools/studies/slice0_guess.py, device PCG recurrence on the
+    // oracle's exact path, config 3: 1.41 -> 1.17 iterations per solve in
+    // slice 0): order 7 through the layer, then 5, then 4 where rounding
+    // amplified by higher orders dominates the residual.  The kernel uses the
+    // table in slice 0 (and in the single-slice sequential solver); rows of
+    // later slices are kept for that solver, whose slice 0 spans the horizon.
     const long rows = (long)nt * m + 1;
     std::vector<double> ext((size_t)rows * 8, 0.0);
-    for (long r = 2; r < rows; ++r) {
-      const int p = (int)std::min<long>(r - 1, pf::EXO);
-      long double tau[pf::EXO + 1];
-      for (int j = 0; j <= p; ++j) tau[j] = powl((long double)(r - 1 - j) * (long double)c->dt, (long double)alpha);
-      const long double tr = powl((long double)r * (long double)c->dt, (long double)alpha);
+    auto order = [](long r, bool first) -> int {
+      if (first) return r < 16 ? 5 : r < 64 ? 7 : r < 128 ? 6 : r < 256 ? 5 : 4;
+      return r < 8 ? 3 : r < 16 ? 4 : r < 128 ? 7 : 5;
+    };
+    for (long k = 2; k < rows; ++k) {
+      const long r = (k - 1) % m + 1;  // local substep of target k (slice (k - 1) / m)
+      if (r < 2 && m > 1) continue;
+      const long rr = m > 1 ? r : k;
+      const int p = (int)std::min<long>(std::min<long>(rr - 1, pf::EXT), order(rr, (k - 1) / m == 0));
+      long double tau[pf::EXT + 1];
+      for (int j = 0; j <= p; ++j) tau[j] = powl((long double)(k - 1 - j) * (long double)c->dt, (long double)alpha);
+      const long double tr = powl((long double)k * (long double)c->dt, (long double)alpha);
       for (int j = 0; j <= p; ++j) {
         long double w = 1.0L;
         for (int q = 0; q <= p; ++q)
           if (q != j) w *= (tr - tau[q]) / (tau[j] - tau[q]);
-        ext[(size_t)r * 8 + j] = (double)w;
+        ext[(size_t)k * 8 + j] = (double)w;
       }
     }
     PF_CUDA(c, cudaMalloc(&c->d_ext0, sizeof(double) * ext.size()));
@@ -578,7 +613,7 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
 void pf_destroy(pf_ctx* c) {
   if (!c) return;
   if (c->device >= 0) cudaSetDevice(c->device);
-  for (DevBuf* b : {&c->U, &c->Unext, &c->paths, &c->fold, &c->gold, &c->gnew, &c->io, &c->scalar, &c->scratch,
+  for (DevBuf* b : {&c->U, &c->Unext, &c->paths, &c->fold, &c->gold, &c->gnew, &c->io, &c->scalar, &c->scratch, &c->brk,
                     &c->wpaths[0], &c->wpaths[1]})
     b->release();
   for (void* p : {(void*)c->d_bfine, (void*)c->d_afine, (void*)c->d_bfrac, (void*)c->d_ext0, (void*)c->d_nodes, (void*)c->d_d1, (void*)c->d_qw,

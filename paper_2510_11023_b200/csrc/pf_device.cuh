@@ -10,11 +10,24 @@ namespace pf {
 // Optional phase timing of slice 0 (build with -DPF_PHASE_TIMING; read with
 // pf_debug_phases).  Compiled out of the product library.
 #ifdef PF_PHASE_TIMING
+#ifndef PF_PHASE_SLICE
+#define PF_PHASE_SLICE 0
+#endif
 __device__ long long g_phase[16];
 __device__ long long g_phase_last;
+__device__ long long g_phase_last_h;
+// helper CTA of slice PF_PHASE_SLICE (uses the kernel's `helper` and `b`)
+#define PF_TH(k)                                                     \
+  do {                                                               \
+    if (threadIdx.x == 0 && helper && b == PF_PHASE_SLICE) {         \
+      const long long _t = clock64();                                \
+      g_phase[(k)] += _t - g_phase_last_h;                           \
+      g_phase_last_h = _t;                                           \
+    }                                                                \
+  } while (0)
 #define PF_T(k)                                        \
   do {                                                 \
-    if (threadIdx.x == 0 && blockIdx.x == 0) {         \
+    if (threadIdx.x == 0 && blockIdx.x == PF_PHASE_SLICE) { \
       const long long _t = clock64();                  \
       g_phase[(k)] += _t - g_phase_last;               \
       g_phase_last = _t;                               \
@@ -23,6 +36,9 @@ __device__ long long g_phase_last;
 #else
 #define PF_T(k) \
   do {          \
+  } while (0)
+#define PF_TH(k) \
+  do {           \
   } while (0)
 #endif
 
@@ -49,6 +65,7 @@ struct Status {
   int iters;  // PCG iterations accumulated by this CTA
   int solves; // linear solves performed by this CTA
   int pad[2];
+  long long t_start, t_end;  // fine-sweep slice CTAs: globaltimer at entry / exit (load-balance diagnostic)
 };
 
 // ---------------------------------------------------------------------------

@@ -23,7 +23,10 @@ struct Common {
   const double* bfine;                // b_q
   const double* afine;                // a_s = b_{s-1} - b_s (s >= 1; a_0 unused)
   const double* bfrac;                // b_{q/m}
-  double* scratch;                    // per-slice block history / bracket rows
+  double* scratch;                    // per-slice block history rows
+  // coarse-history bracket of every (slice, substep), precomputed by
+  // k_bracket_all: (nslices, m, size), row r-1 = target substep r; nullptr = 0
+  const double* brk;
   double anear[16];                   // a_s for s < 16 (near-history weights, uniform loads)
   // slice-0 PCG guess: Lagrange extrapolation in tau = t^alpha (the t^alpha
   // initial layer defeats polynomial extrapolation in t), 8 weights per r
@@ -39,6 +42,9 @@ constexpr int NR = 2 * HB;
 // PCG initial guess: order-EXO polynomial extrapolation of the path,
 // x0 = sum_j (-1)^j C(p+1, j+1) c_{r-1-j}, p = min(EXO, r-1).
 constexpr int EXO = 5;
+// Tabulated guesses (Common::ext0, 1-D with alpha < 1): Lagrange extrapolation
+// in tau = t^alpha of order <= EXT, host-scheduled per substep (see pf_create).
+constexpr int EXT = 7;
 // kExtrap[p][j] = (-1)^j C(p+1, j+1)
 __constant__ double kExtrap[EXO + 1][EXO + 1] = {
     {1, 0, 0, 0, 0, 0},        {2, -1, 0, 0, 0, 0},        {3, -3, 1, 0, 0, 0},
@@ -121,58 +127,37 @@ __device__ __forceinline__ void far_history_block(const Common& c, const double*
     }
 }
 
-// Coarse-history bracket rows for r = r0 .. r0+HB-1 of slice n
-// (stepping.py:124-139): -m^-alpha sum_{j<n} b_{j + r/m} (U_{n-j} - U_{n-j-1}).
-template <int NT, int EPT>
-__device__ __forceinline__ void bracket_block(const Common& c, const double* __restrict__ U, int n, int r0,
-                                              double* out) {
-  double acc[HB][EPT];
+// Coarse-history bracket (stepping.py:124-139, _coarse_contribution)
+//   -m^-alpha sum_{j<n} b_{j + r/m} (U_{n-j} - U_{n-j-1})
+// of every (slice, substep) of a sweep, before it starts: the A2 GEMM of
+// SURVEY §8(a) (picks^T x dU per slice), j ascending with one fma per (j, row)
+// per element (deterministic; previously done block by block on the helper
+// CTAs, where it made the helpers of late slices -- n coarse rows each -- the
+// critical path).  Thread: one mode, RT consecutive target rows; grid
+// (modes / 256, m / RT, slices).
+template <int RT>
+__global__ void __launch_bounds__(256) k_bracket_all(Common c, const double* __restrict__ U, int n_lo,
+                                                     double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r0 = blockIdx.y * RT + 1;
+  const int b = blockIdx.z, n = n_lo + b;
+  if (e >= c.size) return;
+  double acc[RT];
 #pragma unroll
-  for (int rr = 0; rr < HB; ++rr)
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) acc[rr][i] = 0.0;
+  for (int q = 0; q < RT; ++q) acc[q] = 0.0;
+  double hi = U[(size_t)n * c.size + e];
   for (int j = 0; j < n; ++j) {
-    double inc[EPT];
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int e = threadIdx.x + i * NT;
-      inc[i] = (e < c.size) ? U[(size_t)(n - j) * c.size + e] - U[(size_t)(n - j - 1) * c.size + e] : 0.0;
-    }
+    const double lo = U[(size_t)(n - j - 1) * c.size + e];
+    const double inc = hi - lo;
+    hi = lo;
     const double* w = c.bfrac + (size_t)j * c.m + r0;
 #pragma unroll
-    for (int rr = 0; rr < HB; ++rr) {
-      const double wr = w[rr];
-#pragma unroll
-      for (int i = 0; i < EPT; ++i) acc[rr][i] = fma(wr, inc[i], acc[rr][i]);
-    }
+    for (int q = 0; q < RT; ++q)
+      if (r0 + q <= c.m) acc[q] = fma(w[q], inc, acc[q]);
   }
 #pragma unroll
-  for (int rr = 0; rr < HB; ++rr)
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int e = threadIdx.x + i * NT;
-      if (e < c.size) out[(size_t)rr * c.size + e] = (n > 0) ? -c.minv * acc[rr][i] : 0.0;
-    }
-}
-
-// coarse-history bracket of slice n for target (n, r)  (stepping.py:124-139):
-//   -m^-alpha sum_{j=0}^{n-1} b_{j + r/m} (U_{n-j} - U_{n-j-1})
-template <int NT, int EPT>
-__device__ __forceinline__ void coarse_bracket(const Common& c, const double* __restrict__ U, int n, int r,
-                                               double* ct) {
-#pragma unroll
-  for (int i = 0; i < EPT; ++i) {
-    const int e = threadIdx.x + i * NT;
-    double s = 0.0;
-    if (e < c.size && n > 0) {
-      for (int j = 0; j < n; ++j) {
-        const double inc = U[(size_t)(n - j) * c.size + e] - U[(size_t)(n - j - 1) * c.size + e];
-        s = fma(c.bfrac[(size_t)j * c.m + r], inc, s);
-      }
-      s = -c.minv * s;
-    }
-    ct[i] = s;
-  }
+  for (int q = 0; q < RT; ++q)
+    if (r0 + q <= c.m) out[((size_t)b * c.m + r0 - 1 + q) * c.size + e] = (n > 0) ? -c.minv * acc[q] : 0.0;
 }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -228,13 +213,18 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
                                                    double* __restrict__ out, Status* __restrict__ status) {
   extern __shared__ __align__(16) char smem[];
   constexpr int JT = (EPT > 2 ? 4 : 8);  // rows per register chunk (x2 double-buffered)
-  const bool helper = (int)blockIdx.x >= nslices;
+#ifndef PF_INTERLEAVE
+#define PF_INTERLEAVE 0
+#endif
+  // PF_INTERLEAVE (one helper per slice): slice b at block 2b, its helper at 2b + 1
+  const bool il = PF_INTERLEAVE && helpers == 1;
+  const bool helper = il ? ((int)blockIdx.x & 1) != 0 : (int)blockIdx.x >= nslices;
   // `helpers` = helper CTAs per slice (0: far history inline).  With K > 1 the
   // far-history rows are split by row blocks (block rb -> helper rb mod K) and
   // the slice CTA sums the K partial tiles in fixed order (split-K).
   const int hps = helpers > 0 ? helpers : 1;
-  const int b = helper ? ((int)blockIdx.x - nslices) / hps : (int)blockIdx.x;
-  const int hid = helper ? ((int)blockIdx.x - nslices) % hps : 0;
+  const int b = il ? (int)blockIdx.x >> 1 : helper ? ((int)blockIdx.x - nslices) / hps : (int)blockIdx.x;
+  const int hid = il ? 0 : helper ? ((int)blockIdx.x - nslices) % hps : 0;
   const int n = n_lo + b;
   double* path = paths + (size_t)b * (c.m + 1) * c.size;
   // per slice: [parity][hps + 1][hist | bracket][HB][size]; tile hps is the combined one
@@ -252,6 +242,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     }
     for (int beta = 0; beta < nblocks; ++beta) {
       const int J = far_extent(beta);
+      PF_TH(14);
       if (J > 0) {
         if (threadIdx.x == 0) {
           int ns = 64;
@@ -263,6 +254,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         __syncthreads();
         if (ld_acquire(sync.abort + b) != 0) return;
       }
+      PF_TH(11);
       double* hs = slot(beta & 1, hid);
       const int R0 = beta * HB;
       // this helper's rows: blocks rb = hid, hid + hps, ... of HB rows starting at row 1
@@ -298,10 +290,16 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
           const int e = threadIdx.x + i * NT;
           if (e < c.size) hs[(size_t)rr * c.size + e] = acc[rr][i];
         }
-      if (hid == 0) bracket_block<NT, EPT>(c, U, n, R0 + 1, hs + (size_t)HB * c.size);
+      PF_TH(12);
       cta_publish(sync.ready + b * hps + hid, beta + 1);
     }
     return;
+  }
+  long long t_entry = 0;
+  if (threadIdx.x == 0) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    t_entry = (long long)t0;
   }
   SP sp;
   sp.init(smem, spp);
@@ -311,7 +309,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   __shared__ double s_anear[16];
   if (threadIdx.x < 16) s_anear[threadIdx.x] = c.anear[threadIdx.x];
   __syncthreads();
-  Status st = {ST_OK, n, 0, -1, 0, 0, {0, 0}};
+  Status st = {ST_OK, n, 0, -1, 0, 0, {0, 0}, 0, 0};
   double x[EPT];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
@@ -325,11 +323,20 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   const double* hs = nullptr;
   int J = 0;
   double hnext[EPT], cnext[EPT];  // this block's far rows, prefetched one substep ahead
-  // slice-0 tau-extrapolation weights, prefetched one substep ahead (uniform loads)
-  const bool tau_guess = (n == 0 && c.ext0 != nullptr);
-  double wnext[EXO + 1];
+  const double* brk_b = c.brk ? c.brk + (size_t)b * c.m * c.size : nullptr;
 #pragma unroll
-  for (int j = 0; j <= EXO; ++j) wnext[j] = tau_guess && c.m >= 2 ? c.ext0[(size_t)2 * 8 + j] : 0.0;
+  for (int i = 0; i < EPT; ++i) {
+    const int e = threadIdx.x + i * NT;
+    cnext[i] = (brk_b && e < c.size) ? __ldcg(brk_b + e) : 0.0;
+  }
+  // slice-0 tau-extrapolation weights, prefetched one substep ahead (uniform loads)
+  // tabulated guess weights of slice 0's substeps (the t^alpha initial layer;
+  // the other slices use kExtrap: measured faster), prefetched one substep ahead
+  const bool tau_guess = n == 0 && c.ext0 != nullptr;
+  const double* ext = tau_guess ? c.ext0 + (size_t)n * c.m * 8 : nullptr;
+  double wnext[EXT + 1];
+#pragma unroll
+  for (int j = 0; j <= EXT; ++j) wnext[j] = tau_guess && c.m >= 2 ? ext[(size_t)2 * 8 + j] : 0.0;
   for (int r = 1; r <= c.m; ++r) {
     const double t = (double)n * c.dT + (double)(r - 1) * c.dt;
     const int rr = (r - 1) % HB;
@@ -368,14 +375,12 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         }
       } else {
         far_history_block<NT, EPT, JT>(c, path, c.afine, beta * HB, J, s0);
-        bracket_block<NT, EPT>(c, U, n, r, s0 + (size_t)HB * c.size);
       }
       hs = s0;
 #pragma unroll
       for (int i = 0; i < EPT; ++i) {
         const int e = threadIdx.x + i * NT;
         hnext[i] = (e < c.size) ? __ldcg(hs + e) : 0.0;
-        cnext[i] = (e < c.size) ? __ldcg(hs + (size_t)HB * c.size + e) : 0.0;
       }
     }
     PF_T(8);
@@ -390,16 +395,23 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       for (int i = 0; i < EPT; ++i) {
         const int e = threadIdx.x + i * NT;
         hnext[i] = (e < c.size) ? __ldcg(hs + (size_t)(rr + 1) * c.size + e) : 0.0;
-        cnext[i] = (e < c.size) ? __ldcg(hs + (size_t)(HB + rr + 1) * c.size + e) : 0.0;
       }
     }
-    const int p = r - 1 < EXO ? r - 1 : EXO;
-    double wcur[EXO + 1];
-    const bool use_tau = tau_guess && r >= 2;
+    if (r < c.m) {  // next substep's bracket row, landing during this step
 #pragma unroll
-    for (int j = 0; j <= EXO; ++j) {
-      wcur[j] = use_tau ? wnext[j] : kExtrap[p][j];
-      if (use_tau && r + 1 <= c.m) wnext[j] = c.ext0[(size_t)(r + 1) * 8 + j];
+      for (int i = 0; i < EPT; ++i) {
+        const int e = threadIdx.x + i * NT;
+        cnext[i] = (brk_b && e < c.size) ? __ldcg(brk_b + (size_t)r * c.size + e) : 0.0;
+      }
+    }
+    const bool use_tau = tau_guess && r >= 2;
+    const int pk = r - 1 < EXO ? r - 1 : EXO;
+    const int p = use_tau ? (r - 1 < EXT ? r - 1 : EXT) : pk;  // tabulated rows are zero beyond their order
+    double wcur[EXT + 1];
+#pragma unroll
+    for (int j = 0; j <= EXT; ++j) {
+      wcur[j] = use_tau ? wnext[j] : (j <= EXO ? kExtrap[pk][j] : 0.0);
+      if (use_tau && r + 1 <= c.m) wnext[j] = ext[(size_t)(r + 1) * 8 + j];
     }
     double h[EPT], ct[EPT], xg[EPT], xn[EPT];
 #pragma unroll
@@ -422,7 +434,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
           for (int q = 1; q < NR; ++q)
             if (r - q > J) acc = fma(s_anear[q], v[q - 1], acc);
 #pragma unroll
-          for (int j = 1; j <= EXO; ++j)
+          for (int j = 1; j <= EXT; ++j)
             if (j <= p) g = fma(w[j], v[j], g);
         } else {
           for (int j = J + 1; j < r; ++j) acc = fma(s_anear[r - j], path[(size_t)j * c.size + e], acc);
@@ -459,7 +471,13 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   } else if (helpers && threadIdx.x == 0) {
     st_release(sync.abort + b, 1);
   }
-  if (threadIdx.x == 0) status[b] = st;
+  if (threadIdx.x == 0) {
+    unsigned long long tend;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tend));
+    st.t_start = t_entry;
+    st.t_end = (long long)tend;
+    status[b] = st;
+  }
 }
 
 // coarse step G(H[0..n]) -> x  (stepping.py:87-112)
@@ -511,7 +529,7 @@ __global__ void __launch_bounds__(NT) k_coarse(Common c, SPP spp, CoarseArgs a, 
   extern __shared__ __align__(16) char smem[];
   SP sp;
   sp.init(smem, spp);
-  Status st = {ST_OK, 0, -1, -1, 0, 0, {0, 0}};
+  Status st = {ST_OK, 0, -1, -1, 0, 0, {0, 0}, 0, 0};
   double x[EPT];
   if (a.mode == CM_SINGLE) {
     st.n = a.n_single;
