@@ -245,10 +245,12 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       PF_TH(14);
       if (J > 0) {
         if (threadIdx.x == 0) {
-          int ns = 64;
+          // short backoff: the slice CTA publishes once per block and every
+          // microsecond of oversleep here delays the block it will wait for
+          int ns = 32;
           while (ld_acquire(sync.progress + b) < J && ld_acquire(sync.abort + b) == 0) {
             __nanosleep(ns);
-            ns = ns < 2048 ? 2 * ns : ns;
+            ns = ns < 256 ? 2 * ns : ns;
           }
         }
         __syncthreads();
@@ -349,10 +351,10 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         cta_publish(sync.progress + b, r - 1);  // rows 0..r-1 are in the path
         if (threadIdx.x == 0) {
           for (int h = 0; h < hps; ++h) {
-            int ns = 64;
+            int ns = 32;
             while (ld_acquire(sync.ready + b * hps + h) < beta + 1) {
               __nanosleep(ns);
-              ns = ns < 2048 ? 2 * ns : ns;
+              ns = ns < 256 ? 2 * ns : ns;
             }
           }
         }

@@ -27,12 +27,14 @@ RAW = ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__dram_throughput.av
 
 
 def main(tag):
-    for src, dst in (("bench", "bench"), ("bench_ref", "bench_ref"), ("bench_c2", "bench_c2"), ("bench_c4", "bench_c4")):
+    for src, dst in (("bench", "bench"), ("bench_ref", "bench_ref"), ("bench_c2", "bench_c2"), ("bench_c4", "bench_c4"),
+                     ("bench_c5", "bench_c5"), ("bench_dist1", "bench_dist1_nccl")):
         f = os.path.join(G, f"{src}_{tag}.json")
         if os.path.exists(f):
             shutil.copy(f, os.path.join(P, f"{tag}_{dst}.json"))
     for src, dst in (("pytest_gpu", "pytest_gpu.txt"), ("phases", "phases_slice0_config3.txt"),
-                     ("slices", "per_slice_config3.txt"), ("smoke", "smoke.txt")):
+                     ("slices", "per_slice_config3.txt"), ("smoke", "smoke.txt"),
+                     ("finish", "slice_finish_config3.txt")):
         f = os.path.join(G, f"{src}_{tag}.txt")
         if os.path.exists(f):
             shutil.copy(f, os.path.join(P, f"{tag}_{dst}"))
