@@ -138,23 +138,35 @@ __device__ __forceinline__ void far_history_block(const Common& c, const double*
 template <int RT>
 __global__ void __launch_bounds__(256) k_bracket_all(Common c, const double* __restrict__ U, int n_lo,
                                                      double* __restrict__ out) {
+  constexpr int JC = 64;  // weights b_{j + r/m} of JC coarse rows x RT target rows staged in shared memory
+  __shared__ double sw[JC][RT];
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const int r0 = blockIdx.y * RT + 1;
   const int b = blockIdx.z, n = n_lo + b;
-  if (e >= c.size) return;
+  const bool live = e < c.size;
   double acc[RT];
 #pragma unroll
   for (int q = 0; q < RT; ++q) acc[q] = 0.0;
-  double hi = U[(size_t)n * c.size + e];
-  for (int j = 0; j < n; ++j) {
-    const double lo = U[(size_t)(n - j - 1) * c.size + e];
-    const double inc = hi - lo;
-    hi = lo;
-    const double* w = c.bfrac + (size_t)j * c.m + r0;
+  double hi = live ? U[(size_t)n * c.size + e] : 0.0;
+  for (int j0 = 0; j0 < n; j0 += JC) {
+    const int jn = min(JC, n - j0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < jn * RT; t += blockDim.x) {
+      const int j = t / RT, q = t % RT;
+      sw[j][q] = r0 + q <= c.m ? c.bfrac[(size_t)(j0 + j) * c.m + r0 + q] : 0.0;
+    }
+    __syncthreads();
+    if (!live) continue;
+#pragma unroll 4
+    for (int j = 0; j < jn; ++j) {
+      const double lo = U[(size_t)(n - j0 - j - 1) * c.size + e];
+      const double inc = hi - lo;
+      hi = lo;
 #pragma unroll
-    for (int q = 0; q < RT; ++q)
-      if (r0 + q <= c.m) acc[q] = fma(w[q], inc, acc[q]);
+      for (int q = 0; q < RT; ++q) acc[q] = fma(sw[j][q], inc, acc[q]);
+    }
   }
+  if (!live) return;
 #pragma unroll
   for (int q = 0; q < RT; ++q)
     if (r0 + q <= c.m) out[((size_t)b * c.m + r0 - 1 + q) * c.size + e] = (n > 0) ? -c.minv * acc[q] : 0.0;
