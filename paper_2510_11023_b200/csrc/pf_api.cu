@@ -219,6 +219,9 @@ int ensure_status(pf_ctx* c, int n) {
 // Launch the fine sweep for slices [n_lo, n_lo+bs) reading device states d_u.
 // When 2*bs CTAs fit on the device at once, launch cooperatively with one
 // helper CTA per slice (far history on otherwise idle SMs); else inline.
+#ifndef PF_BRK_RT
+#define PF_BRK_RT 16
+#endif
 int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, Status* d_st, int m_override = 0,
                 int hps_req = 1) {
   if (c->kind == PF_SPACE_SINE2D) {
@@ -248,7 +251,7 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   cm.brk = nullptr;
   if (n_lo + bs > 1) {  // some slice has a coarse history: its bracket rows, one batched GEMM
     if (c->brk.ensure((size_t)bs * m * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "bracket");
-    constexpr int RT = 16;
+    constexpr int RT = PF_BRK_RT;
     const dim3 gb((unsigned)((c->size + 255) / 256), (unsigned)((m + RT - 1) / RT), (unsigned)bs);
     pf::k_bracket_all<RT><<<gb, 256, 0, c->stream>>>(cm, d_u, n_lo, c->brk.p);
     c->stats.kernel_launches += 1;
