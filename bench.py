@@ -325,7 +325,10 @@ def main():
             "hbm_frac": history_bytes(M ** dims, m, hi - lo) / (ms / 1e3) / 1e9 / peaks.get("hbm_gbs", 6537.0)}
     try:
         with open(os.path.join(ROOT, "profiles", f"dram_config{args.config}.json")) as f:
-            roof["traffic"] = json.load(f).get("dram_bytes_per_launch")
+            dram = json.load(f)
+        roof["traffic"] = dram.get("dram_bytes_per_launch")
+        if dram.get("dominant_kernel"):
+            roof["dominant_kernel"] = dram["dominant_kernel"]
     except OSError:
         pass
 
