@@ -25,8 +25,11 @@
 
 namespace pf {
 
-struct L16 {
-  static constexpr int LG = 8, Q = 256, M = 128, TL = 16, NT = 256;
+// TLV lines per CTA (a half-warp each): 16 for batched sweeps, 4 for batch-1
+// coarse solves (4x the CTAs: the kernels are latency-bound there)
+template <int TLV>
+struct L16T {
+  static constexpr int LG = 8, Q = 256, M = 128, TL = TLV, NT = 16 * TLV;
   static constexpr int LS = Q + 1;  // line stride in cd (odd: staged tile writes are conflict-free)
   static constexpr int STP = TL + 1;  // stage row stride in doubles
   static constexpr double SQ2 = 1.4142135623730951;
@@ -35,6 +38,7 @@ struct L16 {
     return sizeof(cd) * (256 + Q) + (lines > stage ? lines : stage);
   }
 };
+using L16 = L16T<16>;
 
 template <bool INV>
 __device__ __forceinline__ void dft4(cd& a0, cd& a1, cd& a2, cd& a3) {
@@ -141,8 +145,8 @@ __device__ __forceinline__ void l16_setup(char* smem, const Sine2DArgs& a, cd*& 
   T = reinterpret_cast<cd*>(smem);
   ph = T + 256;
   lines = ph + L16::Q;
-  for (int j = threadIdx.x; j < 256; j += L16::NT) T[j] = a.tw16[j];
-  for (int j = threadIdx.x; j < L16::Q; j += L16::NT) ph[j] = a.ph[j];
+  for (int j = threadIdx.x; j < 256; j += blockDim.x) T[j] = a.tw16[j];
+  for (int j = threadIdx.x; j < L16::Q; j += blockDim.x) ph[j] = a.ph[j];
   __syncthreads();
 }
 
@@ -228,9 +232,9 @@ __device__ __forceinline__ void l16_anal_own(const cd (&v)[16], const cd* ph, in
 // ---------------------------------------------------------------------------
 // rows, synthesis (along y): lines k1 -> H[q2][k1] (same contract as k2_rows_syn)
 // ---------------------------------------------------------------------------
-template <bool SETUP>
-__global__ void __launch_bounds__(256) k2_rows_syn16(Sine2DArgs a) {
-  using L = L16;
+template <bool SETUP, int TLV = 16>
+__global__ void __launch_bounds__(16 * TLV) k2_rows_syn16(Sine2DArgs a) {
+  using L = L16T<TLV>;
   extern __shared__ __align__(16) char smem[];
   const int b = blockIdx.y;
   if (!SETUP && a.sc[b * 16 + S_DONE] != 0.0) return;
@@ -341,9 +345,9 @@ __device__ __forceinline__ void l16_pointwise(const Sine2DArgs& a, int q2, doubl
 // ---------------------------------------------------------------------------
 // columns (along x) for lines q2 (same contract as k2_cols)
 // ---------------------------------------------------------------------------
-template <bool SETUP>
-__global__ void __launch_bounds__(256, 2) k2_cols16(Sine2DArgs a) {
-  using L = L16;
+template <bool SETUP, int TLV = 16>
+__global__ void __launch_bounds__(16 * TLV, TLV == 16 ? 2 : 1) k2_cols16(Sine2DArgs a) {
+  using L = L16T<TLV>;
   extern __shared__ __align__(16) char smem[];
   const int b = blockIdx.y;
   if (!SETUP && a.sc[b * 16 + S_DONE] != 0.0) return;
@@ -431,9 +435,9 @@ __global__ void __launch_bounds__(256, 2) k2_cols16(Sine2DArgs a) {
 // ---------------------------------------------------------------------------
 // rows, analysis (along y) for lines k1 (same contract as k2_rows_ana)
 // ---------------------------------------------------------------------------
-template <bool SETUP>
-__global__ void __launch_bounds__(256) k2_rows_ana16(Sine2DArgs a) {
-  using L = L16;
+template <bool SETUP, int TLV = 16>
+__global__ void __launch_bounds__(16 * TLV) k2_rows_ana16(Sine2DArgs a) {
+  using L = L16T<TLV>;
   extern __shared__ __align__(16) char smem[];
   const int b = blockIdx.y;
   if (!SETUP && a.sc[b * 16 + S_DONE] != 0.0) return;

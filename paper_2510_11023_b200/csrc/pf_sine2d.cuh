@@ -961,12 +961,15 @@ __global__ void __launch_bounds__(256) k2_update(Sine2DArgs a) {
   if (pcg_is_last_cta(a, b)) pcg_converge(a, b);
 }
 
-// Per-system scalar reductions: one warp per system sums the M line
-// partials in a fixed order.  kind 0: after SETUP (bb, rr, rz); 1: pq -> alpha;
-// 2: (rr, rz) -> convergence / beta.  Writes the count of unfinished systems.
+// Per-system scalar reductions of a substep's setup: one warp per system sums
+// the line partials in a fixed order.  kind 3: dbar (Q column partials);
+// kind 0: (bb, rr, rz) after the setup analysis, writes the count of
+// unfinished systems.  The per-iteration reductions are pcg_alpha /
+// pcg_converge, fused into the launches that produce their partials.
 __global__ void k2_reduce(Sine2DArgs a, int kind, int maxit, int* remaining) {
   const int b = blockIdx.x;
   const int lane = threadIdx.x;
+  (void)maxit;
   if (kind == 3) {  // dbar = sum over the Q column partials
     double s = 0.0;
     for (int q = lane; q < a.Q; q += 32) s += a.part[((size_t)b * a.Q + q) * 4];
@@ -975,49 +978,21 @@ __global__ void k2_reduce(Sine2DArgs a, int kind, int maxit, int* remaining) {
     return;
   }
   double s[3] = {0.0, 0.0, 0.0};
-  const int slot0 = kind == 1 ? 1 : (kind == 0 ? 1 : 2);
-  const int nval = kind == 0 ? 3 : (kind == 1 ? 1 : 2);
-  if (a.sc[b * 16 + S_DONE] != 0.0 && kind != 0) {
-    return;
-  }
   for (int k = lane; k < a.M; k += 32)
-    for (int v = 0; v < nval; ++v) s[v] += a.part[((size_t)b * a.Q + k) * 4 + slot0 + v];
+    for (int v = 0; v < 3; ++v) s[v] += a.part[((size_t)b * a.Q + k) * 4 + 1 + v];
   for (int v = 0; v < 3; ++v)
     for (int o = 16; o > 0; o >>= 1) s[v] += __shfl_xor_sync(0xffffffffu, s[v], o);
   if (lane != 0) return;
   double* sc = a.sc + b * 16;
-  if (kind == 0) {
-    sc[S_BB] = s[0];
-    sc[S_RR] = s[1];
-    sc[S_RZ] = s[2];
-    sc[S_IT] = 0.0;
-    sc[S_BETA] = 0.0;  // first direction p = z
-    sc[S_THR] = a.tol2 * s[0];
-    sc[S_FAIL] = (!isfinite(s[0]) || !isfinite(s[1])) ? 1.0 : 0.0;
-    sc[S_ZERO] = (s[0] == 0.0) ? 1.0 : 0.0;
-    sc[S_DONE] = (sc[S_FAIL] != 0.0 || s[0] == 0.0 || !(s[1] > sc[S_THR])) ? 1.0 : 0.0;
-  } else if (kind == 1) {
-    const double alpha = sc[S_RZ] / s[0];
-    sc[S_ALPHA] = alpha;
-    if (!isfinite(alpha)) {
-      sc[S_FAIL] = 1.0;
-      sc[S_DONE] = 1.0;
-    }
-  } else {
-    sc[S_IT] += 1.0;
-    if (!isfinite(s[0])) {
-      sc[S_FAIL] = 1.0;
-      sc[S_DONE] = 1.0;
-    } else if (!(s[0] > sc[S_THR])) {
-      sc[S_DONE] = 1.0;
-    } else if (sc[S_IT] >= (double)maxit) {
-      sc[S_FAIL] = 2.0;
-      sc[S_DONE] = 1.0;
-    } else {
-      sc[S_BETA] = s[1] / sc[S_RZ];
-      sc[S_RZ] = s[1];
-    }
-  }
+  sc[S_BB] = s[0];
+  sc[S_RR] = s[1];
+  sc[S_RZ] = s[2];
+  sc[S_IT] = 0.0;
+  sc[S_BETA] = 0.0;  // first direction p = z
+  sc[S_THR] = a.tol2 * s[0];
+  sc[S_FAIL] = (!isfinite(s[0]) || !isfinite(s[1])) ? 1.0 : 0.0;
+  sc[S_ZERO] = (s[0] == 0.0) ? 1.0 : 0.0;
+  sc[S_DONE] = (sc[S_FAIL] != 0.0 || s[0] == 0.0 || !(s[1] > sc[S_THR])) ? 1.0 : 0.0;
   if (sc[S_DONE] == 0.0) atomicAdd(remaining, 1);
 }
 
