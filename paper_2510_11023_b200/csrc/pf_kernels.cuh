@@ -343,14 +343,20 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     const int e = threadIdx.x + i * NT;
     cnext[i] = (brk_b && e < c.size) ? __ldcg(brk_b + e) : 0.0;
   }
-  // slice-0 tau-extrapolation weights, prefetched one substep ahead (uniform loads)
-  // tabulated guess weights of slice 0's substeps (the t^alpha initial layer;
-  // the other slices use kExtrap: measured faster), prefetched one substep ahead
-  const bool tau_guess = n == 0 && c.ext0 != nullptr;
-  const double* ext = tau_guess ? c.ext0 + (size_t)n * c.m * 8 : nullptr;
+  // PCG guess weights tabulated by local substep r (Common::ext0): Lagrange
+  // extrapolation in the slice's own tau = (r dt)^alpha.  Every slice starts
+  // with a t^alpha-like layer in its local time (its fine history restarts at
+  // t_n on top of the coarse bracket): slice 0 uses the table throughout,
+  // later slices for r < TAU_LOCAL_R, then the polynomial kExtrap
+  // (tools/studies/slice_start_guess.py: slice 1 388 -> 214, slice 8 227 ->
+  // 171 PCG iterations over the first 128 substeps).  Prefetched one substep
+  // ahead (uniform loads).
+  constexpr int TAU_LOCAL_R = 128;
+  const double* ext = c.ext0;
+  const int tau_until = ext == nullptr ? 0 : (n == 0 ? c.m + 1 : TAU_LOCAL_R);
   double wnext[EXT + 1];
 #pragma unroll
-  for (int j = 0; j <= EXT; ++j) wnext[j] = tau_guess && c.m >= 2 ? ext[(size_t)2 * 8 + j] : 0.0;
+  for (int j = 0; j <= EXT; ++j) wnext[j] = (2 < tau_until && c.m >= 2) ? ext[(size_t)2 * 8 + j] : 0.0;
   for (int r = 1; r <= c.m; ++r) {
     const double t = (double)n * c.dT + (double)(r - 1) * c.dt;
     const int rr = (r - 1) % HB;
@@ -418,14 +424,14 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         cnext[i] = (brk_b && e < c.size) ? __ldcg(brk_b + (size_t)r * c.size + e) : 0.0;
       }
     }
-    const bool use_tau = tau_guess && r >= 2;
+    const bool use_tau = r >= 2 && r < tau_until;
     const int pk = r - 1 < EXO ? r - 1 : EXO;
     const int p = use_tau ? (r - 1 < EXT ? r - 1 : EXT) : pk;  // tabulated rows are zero beyond their order
     double wcur[EXT + 1];
 #pragma unroll
     for (int j = 0; j <= EXT; ++j) {
       wcur[j] = use_tau ? wnext[j] : (j <= EXO ? kExtrap[pk][j] : 0.0);
-      if (use_tau && r + 1 <= c.m) wnext[j] = ext[(size_t)(r + 1) * 8 + j];
+      if (r + 1 < tau_until && r + 1 <= c.m) wnext[j] = ext[(size_t)(r + 1) * 8 + j];
     }
     double h[EPT], ct[EPT], xg[EPT], xn[EPT];
 #pragma unroll
