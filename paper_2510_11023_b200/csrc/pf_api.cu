@@ -536,7 +536,7 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
   PF_CUDA(c, cudaMalloc(&c->d_afine, sizeof(double) * h_afine.size()));
   PF_CUDA(c, cudaMemcpy(c->d_afine, h_afine.data(), sizeof(double) * h_afine.size(), cudaMemcpyHostToDevice));
   PF_CUDA(c, cudaMemcpy(c->d_bfrac, c->h_bfrac.data(), sizeof(double) * need_frac, cudaMemcpyHostToDevice));
-  if (c->kind == PF_SPACE_SINE1D && alpha < 1.0) {
+  if ((c->kind == PF_SPACE_SINE1D || c->kind == PF_SPACE_SINE2D) && alpha < 1.0) {
     // PCG guess weights of the fine substeps (global index k = n m + r, local
     // r = 1..m): Lagrange extrapolation in tau = t^alpha from the slice's rows
     // r-1 .. r-1-p, tau(k) = (k dt)^alpha.  The order p follows the t^alpha

@@ -1038,6 +1038,7 @@ struct Hist2DArgs {
   double* far;           // (B, 2, HB, MM): [b][0] far history, [b][1] bracket
   const double* old;     // previous parareal sweep's paths of the same slices, or nullptr
   int warm_order;        // order of the drift extrapolation in the warm guess
+  const double* ext;     // local-tau guess weights by substep (Common::ext0 of the 1-D sweep), or nullptr
 };
 
 template <int NT, int EPT>
@@ -1163,6 +1164,13 @@ __global__ void k2_prep(Hist2DArgs h, int r, double* HIST, double* CON, double* 
       for (int j = 0; j <= q; ++j)
         dlt = fma(w[j], path[(size_t)(r - 1 - j) * MM + e] - op[(size_t)(r - 1 - j) * MM + e], dlt);
       g = op[(size_t)r * MM + e] + dlt;
+    } else if (h.ext && r >= 2 && (h.n0 + b == 0 || r < 128)) {
+      // the slice's local t^alpha-like start layer: Lagrange in its own
+      // tau = (r dt)^alpha (as k_fine_sweep; zero weights beyond the row's order)
+      const double* w = h.ext + (size_t)r * 8;
+      const int pt = r - 1 < EXT ? r - 1 : EXT;
+      g = w[0] * path[(size_t)(r - 1) * MM + e];
+      for (int j = 1; j <= pt; ++j) g = fma(w[j], path[(size_t)(r - 1 - j) * MM + e], g);
     } else {
       const double* w = kExtrap[p];
       g = w[0] * path[(size_t)(r - 1) * MM + e];
