@@ -217,7 +217,8 @@ def _config_dict(cfg_id, world, per_gpu=None):
     return {"workload": f"config{cfg_id}: {cfg['dims']}-D sine Galerkin fine sweep", "modes": cfg["modes"],
             "slices_per_gpu": cfg["nt"], "slices_total": cfg["nt"] * world, "fine_steps_per_slice": cfg["m"],
             "alpha": cfg["alpha"], "t_final": cfg["t_final"], "parallelism": f"slices sharded over {world} GPU(s)",
-            "l2": "inputs larger than L2 (history paths > 126 MB)" if cfg_id >= 3 else "inputs fit in L2"}
+            "l2": "inputs larger than L2 (history paths > 126 MB)" if cfg_id >= 3 else "inputs fit in L2",
+            "inputs": "coarse trajectory (run_coarse): the states of parareal's first fine sweep"}
 
 
 # --------------------------------------------------------------------------
@@ -233,6 +234,8 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parareal", action="store_true")
+    ap.add_argument("--tiled-u0", action="store_true",
+                    help="sweep inputs: the initial state in every slice instead of the coarse trajectory")
     ap.add_argument("--dist", action="store_true",
                     help="use the torch.distributed (NCCL) driver even at one rank (exercises the multi-GPU path)")
     args = ap.parse_args()
@@ -272,9 +275,10 @@ def main():
     torch.cuda.set_stream(stream)
     _lib.lib.pf_set_stream(ctx.handle, _lib.C.c_void_p(stream.cuda_stream))
 
-    # untimed inputs of the sweep: the coarse trajectory (1-D); the 2-D coarse
-    # sweep is P sequential PCG solves, so 2-D slices start from the initial state
-    traj = pfb.run_coarse(prob, op, grids) if dims == 1 else np.tile(pfb.initial_state(prob, op), (P + 1, 1))
+    # untimed inputs of the sweep: the coarse trajectory, i.e. the states of
+    # parareal's first fine sweep (--tiled-u0: every slice from the initial state)
+    traj = (np.tile(pfb.initial_state(prob, op), (P + 1, 1)) if args.tiled_u0
+            else pfb.run_coarse(prob, op, grids))
     U = torch.from_numpy(traj).to(f"cuda:{local}")
     out = torch.empty((hi - lo, M ** dims), dtype=torch.float64, device=f"cuda:{local}")
 
@@ -385,7 +389,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE config RNG convention, SURVEY.md §8d)",
-            "config": _config_dict(args.config, world, P_rank), "roofline": roof, "cpu_baseline": cpu,
+            "config": dict(_config_dict(args.config, world, P_rank),
+                           **({"inputs": "initial state in every slice (--tiled-u0)"} if args.tiled_u0 else {})),
+            "roofline": roof, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "parareal": parareal,
         }
         print(json.dumps(line), flush=True)
