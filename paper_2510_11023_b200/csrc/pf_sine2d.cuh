@@ -1027,6 +1027,9 @@ __global__ void k2_zero_fix(Sine2DArgs a) {
 // history for batched slices (2-D): same blocked Toeplitz GEMM as 1-D, tiled
 // over modes.  far[b][rr][e] (HB rows) and bracket rows for block beta.
 // ---------------------------------------------------------------------------
+#ifndef PF_TAU2D_R
+#define PF_TAU2D_R 32  // substeps of a slice extrapolated in local tau (k2_prep; 16-128 measured, 32 best)
+#endif
 struct Hist2DArgs {
   int MM, m, n0;
   const double* bfine;
@@ -1164,7 +1167,7 @@ __global__ void k2_prep(Hist2DArgs h, int r, double* HIST, double* CON, double* 
       for (int j = 0; j <= q; ++j)
         dlt = fma(w[j], path[(size_t)(r - 1 - j) * MM + e] - op[(size_t)(r - 1 - j) * MM + e], dlt);
       g = op[(size_t)r * MM + e] + dlt;
-    } else if (h.ext && r >= 2 && (h.n0 + b == 0 || r < 128)) {
+    } else if (h.ext && r >= 2 && (h.n0 + b == 0 || r < PF_TAU2D_R)) {
       // the slice's local t^alpha-like start layer: Lagrange in its own
       // tau = (r dt)^alpha (as k_fine_sweep; zero weights beyond the row's order)
       const double* w = h.ext + (size_t)r * 8;
