@@ -548,8 +548,24 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
     // later slices are kept for that solver, whose slice 0 spans the horizon.
     const long rows = (long)nt * m + 1;
     std::vector<double> ext((size_t)rows * 8, 0.0);
-    auto order = [](long r, bool first) -> int {
-      if (first) return r < 16 ? 5 : r < 64 ? 7 : r < 128 ? 6 : r < 256 ? 5 : 4;
+    // order schedule of the first slice (the rows every slice reads by local r):
+    // pairs (order, until r); PF_EXT_SCHED="o1,r1,o2,r2,...,o_last" overrides it
+    // (development aid for re-tuning)
+    std::vector<long> sched = {5, 16, 7, 64, 6, 128, 5, 256, 4};
+    if (const char* es = std::getenv("PF_EXT_SCHED")) {
+      sched.clear();
+      for (const char* q = es; *q;) {
+        sched.push_back(std::strtol(q, const_cast<char**>(&q), 10));
+        if (*q == ',') ++q;
+      }
+      if (sched.empty()) sched = {5};
+    }
+    auto order = [&sched](long r, bool first) -> int {
+      if (first) {
+        size_t i = 0;
+        while (i + 1 < sched.size() && r >= sched[i + 1]) i += 2;
+        return (int)sched[i];
+      }
       return r < 8 ? 3 : r < 16 ? 4 : r < 128 ? 7 : 5;
     };
     for (long k = 2; k < rows; ++k) {
