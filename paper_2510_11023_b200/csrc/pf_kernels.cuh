@@ -351,7 +351,10 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   // (tools/studies/slice_start_guess.py: slice 1 388 -> 214, slice 8 227 ->
   // 171 PCG iterations over the first 128 substeps).  Prefetched one substep
   // ahead (uniform loads).
-  constexpr int TAU_LOCAL_R = 128;
+#ifndef PF_TAU1D_R
+#define PF_TAU1D_R 128
+#endif
+  constexpr int TAU_LOCAL_R = PF_TAU1D_R;
   const double* ext = c.ext0;
   const int tau_until = ext == nullptr ? 0 : (n == 0 ? c.m + 1 : TAU_LOCAL_R);
   double wnext[EXT + 1];
