@@ -537,15 +537,14 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
   PF_CUDA(c, cudaMemcpy(c->d_afine, h_afine.data(), sizeof(double) * h_afine.size(), cudaMemcpyHostToDevice));
   PF_CUDA(c, cudaMemcpy(c->d_bfrac, c->h_bfrac.data(), sizeof(double) * need_frac, cudaMemcpyHostToDevice));
   if ((c->kind == PF_SPACE_SINE1D || c->kind == PF_SPACE_SINE2D) && alpha < 1.0) {
-    // PCG guess weights of the fine substeps (global index k = n m + r, local
-    // r = 1..m): Lagrange extrapolation in tau = t^alpha from the slice's rows
-    // r-1 .. r-1-p, tau(k) = (k dt)^alpha.  The order p follows the t^alpha
-    // layer (tools/studies/slice0_guess.py, device PCG recurrence on the
-    // oracle's exact path, config 3: 1.41 -> 1.17 iterations per solve in
-    // slice 0): order 7 through the layer, then 5, then 4 where rounding
-    // amplified by higher orders dominates the residual.  The kernel uses the
-    // table in slice 0 (and in the single-slice sequential solver); rows of
-    // later slices are kept for that solver, whose slice 0 spans the horizon.
+    // PCG guess weights by substep k: Lagrange extrapolation in tau = (k dt)^alpha
+    // from rows k-1 .. k-1-p.  Rows k <= m are read by every slice at its local
+    // substep r = k (k_fine_sweep, k2_prep: the slice's own tau); rows k > m
+    // serve the single-slice sequential solver, whose slice spans the horizon.
+    // The order p follows the t^alpha layer (tools/studies/slice0_guess.py,
+    // slice_start_guess.py: device PCG recurrence on the oracle's exact path):
+    // order 7 through the layer, then 5, then 4 where rounding amplified by
+    // higher orders dominates the residual.
     const long rows = (long)nt * m + 1;
     std::vector<double> ext((size_t)rows * 8, 0.0);
     // order schedule of the first slice (the rows every slice reads by local r):

@@ -28,8 +28,9 @@ struct Common {
   // k_bracket_all: (nslices, m, size), row r-1 = target substep r; nullptr = 0
   const double* brk;
   double anear[16];                   // a_s for s < 16 (near-history weights, uniform loads)
-  // slice-0 PCG guess: Lagrange extrapolation in tau = t^alpha (the t^alpha
-  // initial layer defeats polynomial extrapolation in t), 8 weights per r
+  // PCG guess weights by local substep r (8 per row): Lagrange extrapolation
+  // in the slice's own tau = (r dt)^alpha -- slice 0's initial layer and every
+  // later slice's start layer defeat polynomial extrapolation in t
   const double* ext0;
 };
 
