@@ -547,8 +547,8 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
     // higher orders dominates the residual.
     const long rows = (long)nt * m + 1;
     std::vector<double> ext((size_t)rows * 8, 0.0);
-    // order schedule of the first slice (the rows every slice reads by local r):
-    // pairs (order, until r); PF_EXT_SCHED="o1,r1,o2,r2,...,o_last" overrides it
+    // order schedule by substep: pairs (order, until k);
+    // PF_EXT_SCHED="o1,k1,o2,k2,...,o_last" overrides it
     // (development aid for re-tuning)
     std::vector<long> sched = {5, 16, 7, 64, 6, 128, 5, 256, 4};
     if (const char* es = std::getenv("PF_EXT_SCHED")) {
@@ -559,19 +559,13 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
       }
       if (sched.empty()) sched = {5};
     }
-    auto order = [&sched](long r, bool first) -> int {
-      if (first) {
-        size_t i = 0;
-        while (i + 1 < sched.size() && r >= sched[i + 1]) i += 2;
-        return (int)sched[i];
-      }
-      return r < 8 ? 3 : r < 16 ? 4 : r < 128 ? 7 : 5;
+    auto order = [&sched](long r) -> int {
+      size_t i = 0;
+      while (i + 1 < sched.size() && r >= sched[i + 1]) i += 2;
+      return (int)sched[i];
     };
     for (long k = 2; k < rows; ++k) {
-      const long r = (k - 1) % m + 1;  // local substep of target k (slice (k - 1) / m)
-      if (r < 2 && m > 1) continue;
-      const long rr = m > 1 ? r : k;
-      const int p = (int)std::min<long>(std::min<long>(rr - 1, pf::EXT), order(rr, (k - 1) / m == 0));
+      const int p = (int)std::min<long>(std::min<long>(k - 1, pf::EXT), order(k));
       long double tau[pf::EXT + 1];
       for (int j = 0; j <= p; ++j) tau[j] = powl((long double)(k - 1 - j) * (long double)c->dt, (long double)alpha);
       const long double tr = powl((long double)k * (long double)c->dt, (long double)alpha);
