@@ -249,6 +249,7 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   double* dp = c->paths.p;
   PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
   cm.brk = nullptr;
+  if (bs > 65535) return set_error(c, PF_ERR_UNSUPPORTED, "more than 65535 slices in one sweep launch");
   if (n_lo + bs > 1) {  // some slice has a coarse history: its bracket rows, one batched GEMM
     if (c->brk.ensure((size_t)bs * m * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "bracket");
     constexpr int RT = PF_BRK_RT;
@@ -554,7 +555,11 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
     if (const char* es = std::getenv("PF_EXT_SCHED")) {
       sched.clear();
       for (const char* q = es; *q;) {
-        sched.push_back(std::strtol(q, const_cast<char**>(&q), 10));
+        char* end = nullptr;
+        const long v = std::strtol(q, &end, 10);
+        if (end == q) break;  // not a number: stop parsing
+        sched.push_back(std::max(1L, v));
+        q = end;
         if (*q == ',') ++q;
       }
       if (sched.empty()) sched = {5};
