@@ -220,7 +220,10 @@ int ensure_status(pf_ctx* c, int n) {
 // When 2*bs CTAs fit on the device at once, launch cooperatively with one
 // helper CTA per slice (far history on otherwise idle SMs); else inline.
 #ifndef PF_BRK_RT
-#define PF_BRK_RT 16
+#define PF_BRK_RT 16  // target rows per thread of k_bracket_all (8 / 16 / 32 measured: 16)
+#endif
+#ifndef PF_BRK_EM
+#define PF_BRK_EM 2  // modes per thread of k_bracket_all
 #endif
 int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, Status* d_st, int m_override = 0,
                 int hps_req = 1) {
@@ -252,9 +255,9 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   if (bs > 65535) return set_error(c, PF_ERR_UNSUPPORTED, "more than 65535 slices in one sweep launch");
   if (n_lo + bs > 1) {  // some slice has a coarse history: its bracket rows, one batched GEMM
     if (c->brk.ensure((size_t)bs * m * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "bracket");
-    constexpr int RT = PF_BRK_RT;
-    const dim3 gb((unsigned)((c->size + 255) / 256), (unsigned)((m + RT - 1) / RT), (unsigned)bs);
-    pf::k_bracket_all<RT><<<gb, 256, 0, c->stream>>>(cm, d_u, n_lo, c->brk.p);
+    constexpr int RT = PF_BRK_RT, EM = PF_BRK_EM;
+    const dim3 gb((unsigned)((c->size + 256 * EM - 1) / (256 * EM)), (unsigned)((m + RT - 1) / RT), (unsigned)bs);
+    pf::k_bracket_all<RT, EM><<<gb, 256, 0, c->stream>>>(cm, d_u, n_lo, c->brk.p);
     c->stats.kernel_launches += 1;
     cm.brk = c->brk.p;
   }

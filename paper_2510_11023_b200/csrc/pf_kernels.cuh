@@ -136,19 +136,23 @@ __device__ __forceinline__ void far_history_block(const Common& c, const double*
 // CTAs, where it made the helpers of late slices -- n coarse rows each -- the
 // critical path).  Thread: one mode, RT consecutive target rows; grid
 // (modes / 256, m / RT, slices).
-template <int RT>
+template <int RT, int EM>
 __global__ void __launch_bounds__(256) k_bracket_all(Common c, const double* __restrict__ U, int n_lo,
                                                      double* __restrict__ out) {
+  static_assert(RT % 2 == 0, "weights are read in pairs");
   constexpr int JC = 64;  // weights b_{j + r/m} of JC coarse rows x RT target rows staged in shared memory
-  __shared__ double sw[JC][RT];
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ __align__(16) double sw[JC][RT];
+  const int e0 = blockIdx.x * (blockDim.x * EM) + threadIdx.x;  // modes e0 + i * blockDim.x, i < EM
   const int r0 = blockIdx.y * RT + 1;
   const int b = blockIdx.z, n = n_lo + b;
-  const bool live = e < c.size;
-  double acc[RT];
+  double acc[EM][RT], hi[EM];
 #pragma unroll
-  for (int q = 0; q < RT; ++q) acc[q] = 0.0;
-  double hi = live ? U[(size_t)n * c.size + e] : 0.0;
+  for (int i = 0; i < EM; ++i) {
+    const int e = e0 + i * (int)blockDim.x;
+    hi[i] = e < c.size ? U[(size_t)n * c.size + e] : 0.0;
+#pragma unroll
+    for (int q = 0; q < RT; ++q) acc[i][q] = 0.0;
+  }
   for (int j0 = 0; j0 < n; j0 += JC) {
     const int jn = min(JC, n - j0);
     __syncthreads();
@@ -157,20 +161,36 @@ __global__ void __launch_bounds__(256) k_bracket_all(Common c, const double* __r
       sw[j][q] = r0 + q <= c.m ? c.bfrac[(size_t)(j0 + j) * c.m + r0 + q] : 0.0;
     }
     __syncthreads();
-    if (!live) continue;
-#pragma unroll 4
+#pragma unroll 2
     for (int j = 0; j < jn; ++j) {
-      const double lo = U[(size_t)(n - j0 - j - 1) * c.size + e];
-      const double inc = hi - lo;
-      hi = lo;
+      double inc[EM];
 #pragma unroll
-      for (int q = 0; q < RT; ++q) acc[q] = fma(sw[j][q], inc, acc[q]);
+      for (int i = 0; i < EM; ++i) {
+        const int e = e0 + i * (int)blockDim.x;
+        const double lo = e < c.size ? U[(size_t)(n - j0 - j - 1) * c.size + e] : 0.0;
+        inc[i] = hi[i] - lo;
+        hi[i] = lo;
+      }
+      const double2* w2 = reinterpret_cast<const double2*>(sw[j]);
+#pragma unroll
+      for (int q = 0; q < RT; q += 2) {
+        const double2 w = w2[q / 2];
+#pragma unroll
+        for (int i = 0; i < EM; ++i) {
+          acc[i][q] = fma(w.x, inc[i], acc[i][q]);
+          acc[i][q + 1] = fma(w.y, inc[i], acc[i][q + 1]);
+        }
+      }
     }
   }
-  if (!live) return;
 #pragma unroll
-  for (int q = 0; q < RT; ++q)
-    if (r0 + q <= c.m) out[((size_t)b * c.m + r0 - 1 + q) * c.size + e] = (n > 0) ? -c.minv * acc[q] : 0.0;
+  for (int i = 0; i < EM; ++i) {
+    const int e = e0 + i * (int)blockDim.x;
+    if (e >= c.size) continue;
+#pragma unroll
+    for (int q = 0; q < RT; ++q)
+      if (r0 + q <= c.m) out[((size_t)b * c.m + r0 - 1 + q) * c.size + e] = (n > 0) ? -c.minv * acc[i][q] : 0.0;
+  }
 }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
