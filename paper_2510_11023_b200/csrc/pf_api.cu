@@ -79,6 +79,9 @@ struct pf_ctx {
   int status_cap = 0;
   std::vector<Status> h_status;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // head start of slice 0 (launch_fine): its own stream and fork/join events
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   pf_stats stats{};
   pf_error err{};
   double guard = 0;
@@ -245,54 +248,90 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
     PF_CUDA(c, cudaMalloc(&c->d_sync, sizeof(int) * nsync));
     c->sync_cap = nsync;
   }
-  pf::SweepSync sync{c->d_sync, c->d_sync + bs, c->d_sync + bs + bs * hps};
   PF_CUDA(c, cudaMemsetAsync(c->d_sync, 0, sizeof(int) * nsync, c->stream));
   pf::Common cm = make_common(c);
   cm.m = m;
-  double* dp = c->paths.p;
   PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
-  cm.brk = nullptr;
   if (bs > 65535) return set_error(c, PF_ERR_UNSUPPORTED, "more than 65535 slices in one sweep launch");
-  if (n_lo + bs > 1) {  // some slice has a coarse history: its bracket rows, one batched GEMM
-    if (c->brk.ensure((size_t)bs * m * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "bracket");
-    constexpr int RT = PF_BRK_RT, EM = PF_BRK_EM;
-    const dim3 gb((unsigned)((c->size + 256 * EM - 1) / (256 * EM)), (unsigned)((m + RT - 1) / RT), (unsigned)bs);
-    pf::k_bracket_all<RT, EM><<<gb, 256, 0, c->stream>>>(cm, d_u, n_lo, c->brk.p);
+  const size_t scr_stride = (size_t)2 * (hps + 1) * 2 * pf::HB * c->size;  // per-slice scratch (k_fine_sweep)
+  // Launch the sweep of slices [n_lo + s0, n_lo + s0 + ns) (local slices s0..) on stream st:
+  // per-slice sync flags, paths, scratch, outputs and status at the local offsets.
+  auto sweep = [&](int s0, int ns, cudaStream_t st, const double* brk) -> int {
+    pf::Common cl = cm;
+    cl.scratch = c->scratch.p + (size_t)s0 * scr_stride;
+    cl.brk = brk;
+    pf::SweepSync sync{c->d_sync + s0, c->d_sync + bs + (size_t)s0 * hps, c->d_sync + bs + (size_t)bs * hps + s0};
+    double* dp = c->paths.p + (size_t)s0 * (m + 1) * c->size;
+    double* dout = d_out ? d_out + (size_t)s0 * c->size : nullptr;
+    Status* dst = d_st + s0;
+    int nl = n_lo + s0;
+    PF_DISPATCH(c, {
+      auto kern = pf::k_fine_sweep<SP, SPP, NT, EPT>;
+      int per_sm = 0;
+      // shared-memory ring of the last NR states behind the space's own smem
+      const size_t ring_bytes = sizeof(double) * pf::NR * c->size;
+      const size_t base = (c->smem + 15) & ~size_t(15);
+      int ring_off = -1;
+      size_t smem = c->smem;
+      if (base + ring_bytes <= 227 * 1024) {
+        ring_off = (int)base;
+        smem = base + ring_bytes;
+      }
+      PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      PF_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+      int helpers = (c->allow_helpers && bs * (1 + hps) <= per_sm * c->num_sms) ? hps : 0;
+      if (!helpers && hps > 1) return set_error(c, PF_ERR_UNSUPPORTED, "split-K helpers do not fit on the device");
+      int nsl = ns;
+      int smem_total = (int)smem;
+      if (helpers) {
+        void* args[] = {(void*)&cl, (void*)&spp, (void*)&d_u, (void*)&nl, (void*)&nsl, (void*)&helpers,
+                        (void*)&ring_off, (void*)&smem_total, (void*)&sync, (void*)&dp, (void*)&dout, (void*)&dst};
+        PF_CUDA(c, cudaLaunchCooperativeKernel((void*)kern, dim3(ns * (1 + hps)), dim3(NT), args, smem, st));
+      } else {
+        kern<<<ns, NT, smem, st>>>(cl, spp, d_u, nl, nsl, 0, ring_off, smem_total, sync, dp, dout, dst);
+      }
+      c->last_helpers = helpers;
+    });
     c->stats.kernel_launches += 1;
-    cm.brk = c->brk.p;
+    return 0;
+  };
+  // bracket rows of slices [n_lo + s0, n_lo + bs): one batched GEMM (k_bracket_all)
+  auto bracket = [&](int s0, cudaStream_t st) -> int {
+    const int ns = bs - s0;
+    if (n_lo + s0 + ns <= 1) return 0;  // only slice 0: no coarse history
+    if (c->brk.ensure((size_t)ns * m * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "bracket");
+    constexpr int RT = PF_BRK_RT, EM = PF_BRK_EM;
+    const dim3 gb((unsigned)((c->size + 256 * EM - 1) / (256 * EM)), (unsigned)((m + RT - 1) / RT), (unsigned)ns);
+    pf::k_bracket_all<RT, EM><<<gb, 256, 0, st>>>(cm, d_u, n_lo + s0, c->brk.p);
+    c->stats.kernel_launches += 1;
+    return 0;
+  };
+  // Head start of slice 0: it has no coarse history (no bracket) and is the
+  // slowest slice (its t^alpha layer), so it starts on a side stream while the
+  // bracket kernel of the other slices runs; they follow on the main stream.
+  const char* nohs = std::getenv("PF_NO_HEADSTART");
+  const bool head = n_lo == 0 && bs >= 2 && m_override == 0 && c->allow_helpers && !(nohs && nohs[0] == '1');
+  if (head) {
+    if (!c->side_stream) {
+      PF_CUDA(c, cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+      PF_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      PF_CUDA(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+    PF_CUDA(c, cudaEventRecord(c->ev_fork, c->stream));
+    PF_CUDA(c, cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+    if (sweep(0, 1, c->side_stream, nullptr)) return c->err.code;
+    PF_CUDA(c, cudaEventRecord(c->ev_join, c->side_stream));
+    if (bracket(1, c->stream)) return c->err.code;
+    if (sweep(1, bs - 1, c->stream, c->brk.p)) return c->err.code;
+    PF_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  } else {
+    if (bracket(0, c->stream)) return c->err.code;
+    if (sweep(0, bs, c->stream, (n_lo + bs > 1) ? c->brk.p : nullptr)) return c->err.code;
   }
-  PF_DISPATCH(c, {
-    auto kern = pf::k_fine_sweep<SP, SPP, NT, EPT>;
-    int per_sm = 0;
-    // shared-memory ring of the last NR states behind the space's own smem
-    const size_t ring_bytes = sizeof(double) * pf::NR * c->size;
-    const size_t base = (c->smem + 15) & ~size_t(15);
-    int ring_off = -1;
-    size_t smem = c->smem;
-    if (base + ring_bytes <= 227 * 1024) {
-      ring_off = (int)base;
-      smem = base + ring_bytes;
-    }
-    PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    PF_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-    int helpers = (c->allow_helpers && bs * (1 + hps) <= per_sm * c->num_sms) ? hps : 0;
-    if (!helpers && hps > 1) return set_error(c, PF_ERR_UNSUPPORTED, "split-K helpers do not fit on the device");
-    int nsl = bs;
-    int smem_total = (int)smem;
-    if (helpers) {
-      void* args[] = {(void*)&cm, (void*)&spp, (void*)&d_u, (void*)&n_lo, (void*)&nsl, (void*)&helpers,
-                      (void*)&ring_off, (void*)&smem_total, (void*)&sync, (void*)&dp, (void*)&d_out, (void*)&d_st};
-      PF_CUDA(c, cudaLaunchCooperativeKernel((void*)kern, dim3(bs * (1 + hps)), dim3(NT), args, smem, c->stream));
-    } else {
-      kern<<<bs, NT, smem, c->stream>>>(cm, spp, d_u, n_lo, nsl, 0, ring_off, smem_total, sync, dp, d_out, d_st);
-    }
-    c->last_helpers = helpers;
-    c->stats.helper_launches += helpers ? 1 : 0;
-  });
   PF_CUDA(c, cudaGetLastError());
   PF_CUDA(c, cudaEventRecord(c->ev1, c->stream));
   c->stats.fine_launches += 1;
-  c->stats.kernel_launches += 1;
+  c->stats.helper_launches += c->last_helpers ? 1 : 0;  // one sweep, however many launches
   return 0;
 }
 
@@ -642,6 +681,9 @@ void pf_destroy(pf_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c->e2;
   delete c;
 }
