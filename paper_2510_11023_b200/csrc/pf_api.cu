@@ -310,7 +310,10 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   // slowest slice (its t^alpha layer), so it starts on a side stream while the
   // bracket kernel of the other slices runs; they follow on the main stream.
   const char* nohs = std::getenv("PF_NO_HEADSTART");
-  const bool head = n_lo == 0 && bs >= 2 && m_override == 0 && c->allow_helpers && !(nohs && nohs[0] == '1');
+  // Only where the bracket kernel is long enough to pay for the second launch
+  // (config 3: 2^25 bracket entries; config 2's 2^18 measured slower).
+  const bool big = (double)m * c->size * bs >= 16777216.0;
+  const bool head = big && n_lo == 0 && bs >= 2 && m_override == 0 && c->allow_helpers && !(nohs && nohs[0] == '1');
   if (head) {
     if (!c->side_stream) {
       PF_CUDA(c, cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
