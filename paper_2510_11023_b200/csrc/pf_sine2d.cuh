@@ -1025,8 +1025,13 @@ __global__ void k2_zero_fix(Sine2DArgs a) {
 
 // ---------------------------------------------------------------------------
 // history for batched slices (2-D): same blocked Toeplitz GEMM as 1-D, tiled
-// over modes.  far[b][rr][e] (HB rows) and bracket rows for block beta.
+// over modes.  far[b][rr][e] (HB2 rows) and bracket rows for block beta.
 // ---------------------------------------------------------------------------
+#ifndef PF_HB2
+#define PF_HB2 8
+#endif
+// block length of the 2-D blocked history (k2_far every HB2 substeps; near rows < 2 HB2 in k2_prep)
+constexpr int HB2 = PF_HB2;
 #ifndef PF_TAU2D_R
 #define PF_TAU2D_R 32  // substeps of a slice extrapolated in local tau (k2_prep; 16-128 measured, 32 best)
 #endif
@@ -1038,7 +1043,7 @@ struct Hist2DArgs {
   double minv;
   const double* U;       // coarse states (nt+1, MM)
   const double* paths;   // (B, m+1, MM)
-  double* far;           // (B, 2, HB, MM): [b][0] far history, [b][1] bracket
+  double* far;           // (B, 2, HB2, MM): [b][0] far history, [b][1] bracket
   const double* old;     // previous parareal sweep's paths of the same slices, or nullptr
   int warm_order;        // order of the drift extrapolation in the warm guess
   const double* ext;     // local-tau guess weights by substep (Common::ext0 of the 1-D sweep), or nullptr
@@ -1049,16 +1054,16 @@ __global__ void __launch_bounds__(NT) k2_far(Hist2DArgs h, int beta) {
   // rows are consumed in chunks of CH with their weights staged in shared
   // memory (the same for every thread), RF rows in flight per thread
   constexpr int CH = 64, RF = 8;
-  __shared__ double ws[CH + HB];   // Toeplitz weights a_{R0+1+rr-j} of the chunk
-  __shared__ double wb[CH * HB];   // bracket weights b_{j+(R0+1+rr)/m} of the chunk
+  __shared__ double ws[CH + HB2];   // Toeplitz weights a_{R0+1+rr-j} of the chunk
+  __shared__ double wb[CH * HB2];   // bracket weights b_{j+(R0+1+rr)/m} of the chunk
   const int b = blockIdx.y;
   const int n = h.n0 + b;
   const int e0 = blockIdx.x * NT * EPT;
   const size_t MM = h.MM;
-  const int R0 = beta * HB;
-  const int J = (beta > 0 ? beta - 1 : 0) * HB;
+  const int R0 = beta * HB2;
+  const int J = (beta > 0 ? beta - 1 : 0) * HB2;
   const double* path = h.paths + (size_t)b * (h.m + 1) * MM;
-  double acc[HB][EPT], cb[HB][EPT];
+  double acc[HB2][EPT], cb[HB2][EPT];
   double c0[EPT];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
@@ -1066,7 +1071,7 @@ __global__ void __launch_bounds__(NT) k2_far(Hist2DArgs h, int beta) {
     c0[i] = (e < h.MM) ? path[e] : 0.0;
   }
 #pragma unroll
-  for (int rr = 0; rr < HB; ++rr) {
+  for (int rr = 0; rr < HB2; ++rr) {
     const double w = h.bfine[R0 + rr];
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
@@ -1078,7 +1083,7 @@ __global__ void __launch_bounds__(NT) k2_far(Hist2DArgs h, int beta) {
     const int jn = min(CH, J - j0 + 1);
     const int s0 = R0 + 1 - j0 - (jn - 1);
     __syncthreads();
-    for (int u = threadIdx.x; u < jn - 1 + HB; u += NT) ws[u] = h.afine[s0 + u];
+    for (int u = threadIdx.x; u < jn - 1 + HB2; u += NT) ws[u] = h.afine[s0 + u];
     __syncthreads();
     for (int t0 = 0; t0 < jn; t0 += RF) {
       double v[RF][EPT];
@@ -1093,7 +1098,7 @@ __global__ void __launch_bounds__(NT) k2_far(Hist2DArgs h, int beta) {
       for (int t = 0; t < RF; ++t) {
         if (t0 + t >= jn) break;
 #pragma unroll
-        for (int rr = 0; rr < HB; ++rr) {
+        for (int rr = 0; rr < HB2; ++rr) {
           const double w = ws[rr - (t0 + t) + jn - 1];
 #pragma unroll
           for (int i = 0; i < EPT; ++i) acc[rr][i] = fma(w, v[t][i], acc[rr][i]);
@@ -1101,12 +1106,12 @@ __global__ void __launch_bounds__(NT) k2_far(Hist2DArgs h, int beta) {
       }
     }
   }
-  // coarse bracket rows r = R0+1 .. R0+HB: -m^-a sum_{j<n} b_{j+r/m} (U_{n-j} - U_{n-j-1})
+  // coarse bracket rows r = R0+1 .. R0+HB2: -m^-a sum_{j<n} b_{j+r/m} (U_{n-j} - U_{n-j-1})
   for (int j0 = 0; j0 < n; j0 += CH) {
     const int jn = min(CH, n - j0);
     __syncthreads();
-    for (int u = threadIdx.x; u < jn * HB; u += NT)
-      wb[u] = h.bfrac[(size_t)(j0 + u / HB) * h.m + R0 + 1 + u % HB];
+    for (int u = threadIdx.x; u < jn * HB2; u += NT)
+      wb[u] = h.bfrac[(size_t)(j0 + u / HB2) * h.m + R0 + 1 + u % HB2];
     __syncthreads();
     for (int t0 = 0; t0 < jn; t0 += RF) {
       double v[RF + 1][EPT];  // rows n-j0-t0 .. n-j0-t0-RF
@@ -1121,23 +1126,23 @@ __global__ void __launch_bounds__(NT) k2_far(Hist2DArgs h, int beta) {
       for (int t = 0; t < RF; ++t) {
         if (t0 + t >= jn) break;
 #pragma unroll
-        for (int rr = 0; rr < HB; ++rr) {
-          const double w = wb[(t0 + t) * HB + rr];
+        for (int rr = 0; rr < HB2; ++rr) {
+          const double w = wb[(t0 + t) * HB2 + rr];
 #pragma unroll
           for (int i = 0; i < EPT; ++i) cb[rr][i] = fma(w, v[t][i] - v[t + 1][i], cb[rr][i]);
         }
       }
     }
   }
-  double* out = h.far + (size_t)b * 2 * HB * MM;
+  double* out = h.far + (size_t)b * 2 * HB2 * MM;
 #pragma unroll
-  for (int rr = 0; rr < HB; ++rr)
+  for (int rr = 0; rr < HB2; ++rr)
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int e = e0 + threadIdx.x + i * NT;
       if (e < h.MM) {
         out[(size_t)rr * MM + e] = acc[rr][i];
-        out[(size_t)(HB + rr) * MM + e] = (n > 0) ? -h.minv * cb[rr][i] : 0.0;
+        out[(size_t)(HB2 + rr) * MM + e] = (n > 0) ? -h.minv * cb[rr][i] : 0.0;
       }
     }
 }
@@ -1146,16 +1151,16 @@ __global__ void __launch_bounds__(NT) k2_far(Hist2DArgs h, int beta) {
 __global__ void k2_prep(Hist2DArgs h, int r, double* HIST, double* CON, double* X0) {
   const int b = blockIdx.y;
   const size_t MM = h.MM;
-  const int rr = (r - 1) % HB, beta = (r - 1) / HB;
-  const int J = (beta > 0 ? beta - 1 : 0) * HB;
+  const int rr = (r - 1) % HB2, beta = (r - 1) / HB2;
+  const int J = (beta > 0 ? beta - 1 : 0) * HB2;
   const int p = r - 1 < EXO ? r - 1 : EXO;
   const double* path = h.paths + (size_t)b * (h.m + 1) * MM;
-  const double* far = h.far + (size_t)b * 2 * HB * MM;
+  const double* far = h.far + (size_t)b * 2 * HB2 * MM;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < MM; e += (size_t)gridDim.x * blockDim.x) {
     double acc = far[(size_t)rr * MM + e];
     for (int j = J + 1; j < r; ++j) acc = fma(h.afine[r - j], path[(size_t)j * MM + e], acc);
     HIST[(size_t)b * MM + e] = acc;
-    CON[(size_t)b * MM + e] = far[(size_t)(HB + rr) * MM + e];
+    CON[(size_t)b * MM + e] = far[(size_t)(HB2 + rr) * MM + e];
     double g;
     if (h.old) {
       // warm guess: the previous sweep's state at this substep plus the
