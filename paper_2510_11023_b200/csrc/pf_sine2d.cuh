@@ -1027,6 +1027,9 @@ __global__ void k2_zero_fix(Sine2DArgs a) {
 // history for batched slices (2-D): same blocked Toeplitz GEMM as 1-D, tiled
 // over modes.  far[b][rr][e] (HB2 rows) and bracket rows for block beta.
 // ---------------------------------------------------------------------------
+#ifndef PF_EXO2
+#define PF_EXO2 4  // 3 / 4 / 5 measured: config 4 212 / 210 / 218 ms, config 5 316 / 285 / 281 ms
+#endif
 #ifndef PF_HB2
 #define PF_HB2 8
 #endif
@@ -1153,7 +1156,7 @@ __global__ void k2_prep(Hist2DArgs h, int r, double* HIST, double* CON, double* 
   const size_t MM = h.MM;
   const int rr = (r - 1) % HB2, beta = (r - 1) / HB2;
   const int J = (beta > 0 ? beta - 1 : 0) * HB2;
-  const int p = r - 1 < EXO ? r - 1 : EXO;
+  const int p = r - 1 < PF_EXO2 ? r - 1 : PF_EXO2;  // polynomial guess order after the local-tau range
   const double* path = h.paths + (size_t)b * (h.m + 1) * MM;
   const double* far = h.far + (size_t)b * 2 * HB2 * MM;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < MM; e += (size_t)gridDim.x * blockDim.x) {
