@@ -144,9 +144,11 @@ int pf_coarse_step(pf_ctx* ctx, const double* history, int n_states, int step_in
 int pf_run_coarse(pf_ctx* ctx, const double* u0, double* traj);
 /* stepping.fine_sweep_intervals: u_nodes has (n_states) rows, out (n_hi-n_lo) rows */
 int pf_fine_sweep(pf_ctx* ctx, const double* u_nodes, int n_states, int n_lo, int n_hi, double* out);
-/* stepping.fine_propagate: coarse_history rows 0..n; endpoint (size) and path (m, size) */
-int pf_fine_propagate(pf_ctx* ctx, const double* coarse_history, int n_states, double* endpoint,
-                      double* path);
+/* stepping.fine_propagate: start (size; NULL = coarse_history[n]) seeds path[0]
+ * (stepping.py:170-171), coarse_history rows 0..n feed the bracket; endpoint
+ * (size) and path (m, size) */
+int pf_fine_propagate(pf_ctx* ctx, const double* start, const double* coarse_history, int n_states,
+                      double* endpoint, double* path);
 /* stepping.chain_fine: traj (nt+1) rows */
 int pf_chain_fine(pf_ctx* ctx, const double* u0, double* traj);
 /* stepping.run_fine_sequential: states (nt+1) rows (every m-th fine state) */

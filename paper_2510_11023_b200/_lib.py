@@ -77,7 +77,7 @@ SIGNATURES = {
     "pf_coarse_step": (C.c_int, [C.c_void_p, _dp, C.c_int, C.c_int, _dp]),
     "pf_run_coarse": (C.c_int, [C.c_void_p, _dp, _dp]),
     "pf_fine_sweep": (C.c_int, [C.c_void_p, _dp, C.c_int, C.c_int, C.c_int, _dp]),
-    "pf_fine_propagate": (C.c_int, [C.c_void_p, _dp, C.c_int, _dp, _dp]),
+    "pf_fine_propagate": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int, _dp, _dp]),
     "pf_chain_fine": (C.c_int, [C.c_void_p, _dp, _dp]),
     "pf_fine_sequential": (C.c_int, [C.c_void_p, _dp, _dp]),
     "pf_parareal": (C.c_int, [C.c_void_p, _dp, C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp,
@@ -167,13 +167,13 @@ class Context:
         b_frac = f64(wt.on_grid(m, max(nt - 1, 0) * m + m + 1))
         self._keep += [b_fine, b_frac]
         weights = pf_weights(ptr(b_fine), b_fine.size, ptr(b_frac), b_frac.size, gamma_2_minus(alpha))
+        self.lock = threading.Lock()
         handle = C.c_void_p()
         rc = lib.pf_create(C.byref(prob), C.byref(grid), C.byref(space), C.byref(weights), int(device),
                            C.byref(handle))
         self.handle = handle
         self.size = op.interior_size
         self.nt, self.m = nt, m
-        self.lock = threading.Lock()
         if rc != PF_OK:
             err = self.last_error()
             self.close()
@@ -195,6 +195,14 @@ class Context:
         return {k: getattr(s, k) for k, _ in pf_stats._fields_}
 
     def close(self):
+        lock = getattr(self, "lock", None)
+        if lock is None:
+            self._destroy()
+            return
+        with lock:  # never free device buffers under a call in flight
+            self._destroy()
+
+    def _destroy(self):
         if getattr(self, "handle", None):
             lib.pf_destroy(self.handle)
             self.handle = None
@@ -230,7 +238,9 @@ def context_for(problem, op, grids, device=0):
     ctx = Context(problem, op, grids, device)
     with _CACHE_LOCK:
         _CACHE[key] = ctx
+        # eviction only drops the cache's reference: a caller (or another
+        # thread mid-call under ctx.lock) may still hold the context, which
+        # is destroyed by Context.__del__ once the last reference goes
         while len(_CACHE) > _CACHE_MAX:
-            _, old = _CACHE.popitem(last=False)
-            old.close()
+            _CACHE.popitem(last=False)
     return ctx

@@ -57,7 +57,7 @@ struct Engine2D;  // 2-D sine engine (pf_engine2d.inc)
 }  // namespace
 
 struct pf_ctx {
-  int device = 0;
+  int device = -1;  // set once cudaSetDevice succeeded (pf_destroy touches no device before)
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   pf_problem prob{};
@@ -104,7 +104,7 @@ struct pf_ctx {
 
 namespace {  // 2-D engine entry points (defined in pf_engine2d.inc)
 int e2_fine_sweep(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, int m, bool with_bracket,
-                  double* d_all = nullptr, bool warm = false);
+                  double* d_all = nullptr, bool warm = false, const double* d_start = nullptr);
 int e2_coarse_step(pf_ctx* c, const double* d_H, int n, double* d_out, int guess = 0,
                    const double* gold = nullptr, const double* ucur = nullptr);
 int e2_run_coarse(pf_ctx* c, double* d_traj);
@@ -115,6 +115,7 @@ int e2_correct(pf_ctx* c, const double* ucur, const double* fold, const double* 
 namespace {
 
 int set_error(pf_ctx* c, int code, const char* msg) {
+  c->err = pf_error{};  // no stale step/node fields from an earlier error
   c->err.code = code;
   std::snprintf(c->err.message, sizeof(c->err.message), "%s", msg);
   return code;
@@ -229,11 +230,12 @@ int ensure_status(pf_ctx* c, int n) {
 #define PF_BRK_EM 2  // modes per thread of k_bracket_all
 #endif
 int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, Status* d_st, int m_override = 0,
-                int hps_req = 1) {
+                int hps_req = 1, const double* d_start = nullptr) {
+  if (d_start && bs != 1) return set_error(c, PF_ERR_ARGUMENT, "a start state needs a single-slice sweep");
   if (c->kind == PF_SPACE_SINE2D) {
     // the parareal driver's own sweeps (states == U) warm-start from the previous sweep
-    const bool warm = c->parareal_ready && d_u == c->U.p && m_override == 0;
-    return e2_fine_sweep(c, d_u, n_lo, bs, d_out, c->grid.m, true, nullptr, warm);
+    const bool warm = c->parareal_ready && d_u == c->U.p && m_override == 0 && !d_start;
+    return e2_fine_sweep(c, d_u, n_lo, bs, d_out, c->grid.m, true, nullptr, warm, d_start);
   }
   const int m = m_override > 0 ? m_override : c->grid.m;
   const int hps = std::max(1, hps_req);
@@ -251,6 +253,7 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   PF_CUDA(c, cudaMemsetAsync(c->d_sync, 0, sizeof(int) * nsync, c->stream));
   pf::Common cm = make_common(c);
   cm.m = m;
+  cm.x_start = d_start;
   PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
   if (bs > 65535) return set_error(c, PF_ERR_UNSUPPORTED, "more than 65535 slices in one sweep launch");
   const size_t scr_stride = (size_t)2 * (hps + 1) * 2 * pf::HB * c->size;  // per-slice scratch (k_fine_sweep)
@@ -564,9 +567,9 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
   for (long s = 1; s < need_fine; ++s) h_afine[s] = c->h_bfine[s - 1] - c->h_bfine[s];
   c->len_frac = need_frac;
 
-  c->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaSetDevice");
+  c->device = device;
   PF_CUDA(c, cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   {
     const char* env = std::getenv("PF_NO_HELPERS");
@@ -764,16 +767,22 @@ int pf_fine_sweep(pf_ctx* c, const double* u_nodes, int n_states, int n_lo, int 
   return decode_fine(c, n_lo, bs);
 }
 
-int pf_fine_propagate(pf_ctx* c, const double* hist, int n_states, double* endpoint, double* path) {
+int pf_fine_propagate(pf_ctx* c, const double* start, const double* hist, int n_states, double* endpoint,
+                      double* path) {
   if (!c || !hist || n_states < 1) return PF_ERR_ARGUMENT;
   const int n = n_states - 1;
   if (n >= c->grid.nt) return set_error(c, PF_ERR_ARGUMENT, "interval index outside the grid");
   cudaSetDevice(c->device);
-  if (c->io.ensure((size_t)(n_states + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "io");
+  if (c->io.ensure((size_t)(n_states + 2) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "io");
   double* d_u = c->io.p;
   double* d_out = c->io.p + (size_t)n_states * c->size;
+  double* d_start = nullptr;
   if (upload(c, d_u, hist, (size_t)n_states * c->size)) return c->err.code;
-  int rc = launch_fine(c, d_u, n, 1, d_out, c->d_status);
+  if (start) {  // path[0] = start (stepping.py:170-171); the bracket uses hist
+    d_start = c->io.p + (size_t)(n_states + 1) * c->size;
+    if (upload(c, d_start, start, c->size)) return c->err.code;
+  }
+  int rc = launch_fine(c, d_u, n, 1, d_out, c->d_status, 0, 1, d_start);
   if (rc) return rc;
   if (endpoint && download(c, endpoint, d_out, c->size)) return c->err.code;
   if (path && download(c, path, c->paths.p + c->size, (size_t)c->grid.m * c->size)) return c->err.code;
@@ -1015,7 +1024,13 @@ int pf_parareal(pf_ctx* c, const double* u0, double tol, int k_max, const double
     const int lo = k == 0 ? 0 : c->frozen;
     if (lo < nt) {
       rc = pf_dev_fine_sweep(c, c->U.p, lo, nt, c->fold.p + (size_t)lo * sz);
-      if (rc) return rc;
+      if (rc) {
+        // the reference sweeps the whole block [0, nt) (threads = 1,
+        // parareal.py:75-88) and reports SolverFailure((0, r)); the frozen
+        // prefix start `lo` is an internal optimisation, not part of the payload
+        if (rc == PF_ERR_SOLVER) c->err.step_n = 0;
+        return rc;
+      }
     }
     double diff = 0.0;
     rc = pf_dev_parareal_correct(c, c->fold.p, k, &diff);

@@ -32,6 +32,9 @@ struct Common {
   // in the slice's own tau = (r dt)^alpha -- slice 0's initial layer and every
   // later slice's start layer defeat polynomial extrapolation in t
   const double* ext0;
+  // start state of the (single) slice when it differs from U[n]: fine_propagate's
+  // `start` (stepping.py:170-171, path[0] = start; the bracket still uses U); nullptr = U[n]
+  const double* x_start;
 };
 
 // Block length of the blocked L1 history: each history row is read once per
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       // this helper's rows: blocks rb = hid, hid + hps, ... of HB rows starting at row 1
       double acc[HB][EPT];
       {
-        const double* row0 = J > 0 ? path : U + (size_t)n * c.size;
+        const double* row0 = J > 0 ? path : (c.x_start ? c.x_start : U + (size_t)n * c.size);
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
           const int e = threadIdx.x + i * NT;
@@ -346,10 +349,11 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   __syncthreads();
   Status st = {ST_OK, n, 0, -1, 0, 0, {0, 0}, 0, 0};
   double x[EPT];
+  const double* srow = c.x_start ? c.x_start : U + (size_t)n * c.size;
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int e = threadIdx.x + i * NT;
-    x[i] = (e < c.size) ? U[(size_t)n * c.size + e] : 0.0;
+    x[i] = (e < c.size) ? srow[e] : 0.0;
     if (e < c.size) {
       path[e] = x[i];
       if (ring) ring[e] = x[i];

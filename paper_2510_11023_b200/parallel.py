@@ -21,6 +21,7 @@ tests substitute CPU ops to check the sharding and exchange logic under
 
 from __future__ import annotations
 
+import contextlib
 import time
 
 import numpy as np
@@ -41,7 +42,14 @@ def block_bounds(count, parts):
 
 
 class DeviceOps:
-    """Per-rank device state machine over ``pf_dev_parareal_*`` (C-ABI)."""
+    """Per-rank device state machine over ``pf_dev_parareal_*`` (C-ABI).
+
+    Owns its context (not the process-wide cache: the state machine's buffers
+    and stream binding must not leak into other callers) and a stream; the
+    driver runs inside ``scope()``, which makes that stream torch's current
+    stream only for the duration of the solve, so kernels, NCCL and copies
+    stay ordered without changing the caller's stream afterwards.
+    """
 
     def __init__(self, problem, op, grids, device):
         import torch
@@ -52,14 +60,15 @@ class DeviceOps:
         self.torch = torch
         self._lib = _lib
         self.device = torch.device("cuda", device)
-        self.ctx = _lib.context_for(problem, op, grids, device=device)
+        self.ctx = _lib.Context(problem, op, grids, device=device)
         self.size = op.interior_size
         self.nt = grids.nt
         self.u0 = _lib.f64(initial_state(problem, op))
-        # kernels, NCCL and copies share one non-default stream so they stay ordered
         self.stream = torch.cuda.Stream(device=self.device)
-        torch.cuda.set_stream(self.stream)
         _lib.lib.pf_set_stream(self.ctx.handle, _lib.C.c_void_p(self.stream.cuda_stream))
+
+    def scope(self):
+        return self.torch.cuda.stream(self.stream)
 
     def empty(self, rows):
         return self.torch.empty((rows, self.size), dtype=self.torch.float64, device=self.device)
@@ -128,6 +137,11 @@ class DistributedParareal:
 
     def solve(self, tol=1e-10, k_max=20):
         """``parareal.py:91-155`` across ranks; returns the reference's result fields."""
+        scope = getattr(self.ops, "scope", None)
+        with (scope() if scope is not None else contextlib.nullcontext()):
+            return self._solve(tol, k_max)
+
+    def _solve(self, tol, k_max):
         t0 = time.perf_counter()
         self.ops.init()
         lo, hi = self.bounds[self.rank]

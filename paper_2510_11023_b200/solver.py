@@ -97,10 +97,12 @@ def fine_propagate(start, coarse_history, op, grids, problem):
         raise ValueError("start state disagrees with the last coarse history entry")
     ctx = context_for(problem, op, grids)
     hist = f64(hist)
+    start = f64(start)
     endpoint = np.empty(op.interior_size)
     path = np.empty((grids.m, op.interior_size))
     with ctx.lock:
-        ctx.check(lib.pf_fine_propagate(ctx.handle, ptr(hist), n + 1, ptr(endpoint), ptr(path)))
+        # path[0] = start (stepping.py:170-171): within START_MISMATCH_TOL of hist[n], not equal
+        ctx.check(lib.pf_fine_propagate(ctx.handle, ptr(start), ptr(hist), n + 1, ptr(endpoint), ptr(path)))
     return endpoint, path
 
 
