@@ -636,9 +636,25 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
     const int ntw = std::max(pf::tw_table_size(c->lgQ), 1);
     std::vector<cd> tw(ntw), ph(c->Q);
     const long double PI = 3.141592653589793238462643383279502884L;
-    // per-pass radix-4 twiddles w_r(k) = exp(-2 pi i r k / (4 Ns)), then radix-2 exp(-2 pi i k / (2 Ns))
+    // per-pass radix-4 twiddles w_r(k) = exp(-2 pi i r k / (4 Ns)), then radix-2 exp(-2 pi i k / (2 Ns));
+    // Q = 1024 (1-D): the radix 8-8-4-4 passes' w1 (+ w4) per pass (pf_sine1d.cuh T10_*)
+    auto put10 = [&](int off, int R, int ns, bool w4) {
+      for (int k = 0; k < ns; ++k) {
+        const long double a = -2.0L * PI * (long double)k / (long double)(R * ns);
+        tw[off + k] = {(double)cosl(a), (double)sinl(a)};
+        if (w4) tw[off + ns + k] = {(double)cosl(4.0L * a), (double)sinl(4.0L * a)};
+      }
+    };
+    if (c->lgQ == 10 && c->kind == PF_SPACE_SINE1D) {
+      put10(pf::T10_R8_8, 8, 8, true);
+      put10(pf::T10_R4_64, 4, 64, false);
+      put10(pf::T10_R4_256, 4, 256, false);
+      put10(pf::T10_R4_4, 4, 4, false);
+      put10(pf::T10_R8_16, 8, 16, true);
+      put10(pf::T10_R8_128, 8, 128, true);
+    }
     int off = 0;
-    for (int p = 1, ns = 4; p < c->lgQ / 2; ++p, ns *= 4) {
+    for (int p = 1, ns = 4; c->lgQ != 10 && p < c->lgQ / 2; ++p, ns *= 4) {
       for (int r = 1; r <= 3; ++r)
         for (int k = 0; k < ns; ++k) {
           const long double a = -2.0L * PI * (long double)(r * k) / (4.0L * ns);

@@ -52,6 +52,17 @@ __device__ __forceinline__ cd cmulc(cd a, cd b) {  // a * conj(b)
 __device__ __forceinline__ cd cadd(cd a, cd b) { return {a.x + b.x, a.y + b.y}; }
 __device__ __forceinline__ cd csub(cd a, cd b) { return {a.x - b.x, a.y - b.y}; }
 
+// radix-4 DFT in place (forward: exp(-2 pi i / 4) = -i; INV: conjugate)
+template <bool INV>
+__device__ __forceinline__ void dft4(cd& a0, cd& a1, cd& a2, cd& a3) {
+  const cd t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = csub(a1, a3);
+  const cd mi3 = {t3.y, -t3.x};  // -i t3
+  a0 = cadd(t0, t2);
+  a1 = INV ? csub(t1, mi3) : cadd(t1, mi3);
+  a2 = csub(t0, t2);
+  a3 = INV ? cadd(t1, mi3) : csub(t1, mi3);
+}
+
 // ---------------------------------------------------------------------------
 // status: one word per CTA, decoded on the host into pf_error
 // ---------------------------------------------------------------------------
@@ -187,6 +198,38 @@ struct Reducer {
     }
     buf ^= 1;
     return make_double3(sa, sb, sc);
+  }
+  __device__ __forceinline__ double4 sum4(double a, double b, double c, double d) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+      d += __shfl_xor_sync(0xffffffffu, d, o);
+    }
+    if (NT == 32) {
+      __syncwarp();
+      return make_double4(a, b, c, d);
+    }
+    const int w = threadIdx.x >> 5;
+    double* slot = red + buf * 128;
+    if ((threadIdx.x & 31) == 0) {
+      slot[4 * w] = a;
+      slot[4 * w + 1] = b;
+      slot[4 * w + 2] = c;
+      slot[4 * w + 3] = d;
+    }
+    __syncthreads();
+    double sa = 0.0, sb = 0.0, sc = 0.0, sd = 0.0;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) {
+      sa += slot[4 * i];
+      sb += slot[4 * i + 1];
+      sc += slot[4 * i + 2];
+      sd += slot[4 * i + 3];
+    }
+    buf ^= 1;
+    return make_double4(sa, sb, sc, sd);
   }
   __device__ __forceinline__ double sum(double a) { return sum2(a, 0.0).x; }
   __device__ __forceinline__ double max(double a) {

@@ -40,16 +40,6 @@ struct L16T {
 };
 using L16 = L16T<16>;
 
-template <bool INV>
-__device__ __forceinline__ void dft4(cd& a0, cd& a1, cd& a2, cd& a3) {
-  const cd t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = csub(a1, a3);
-  const cd mi3 = {t3.y, -t3.x};  // -i t3
-  a0 = cadd(t0, t2);
-  a1 = INV ? csub(t1, mi3) : cadd(t1, mi3);
-  a2 = csub(t0, t2);
-  a3 = INV ? cadd(t1, mi3) : csub(t1, mi3);
-}
-
 // multiply by w16^m (forward w = exp(-2 pi i / 16); INV: conjugate), m in {1,2,3,4,6,9}
 template <bool INV, int MM>
 __device__ __forceinline__ cd w16mul(cd a) {

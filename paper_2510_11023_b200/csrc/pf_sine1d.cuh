@@ -34,7 +34,13 @@ struct Sine1DParams {
   int pcg_maxit;
 };
 
+// Q = 1024 (config 3) runs radix 8-8-4 | 4 passes instead of radix-4 (see r8_pass10):
+// its twiddle table holds w1 (and w4 for radix-8 passes) per (radix, Ns) pass.
+constexpr int T10_R8_8 = 0, T10_R4_64 = 16, T10_R4_256 = 80, T10_R4_4 = 336, T10_R8_16 = 340,
+              T10_R8_128 = 372, T10_SIZE = 628;
+
 __host__ __device__ constexpr int tw_table_size(int lg) {
+  if (lg == 10) return T10_SIZE;
   int n = 0, ns = 4;
   for (int p = 1; p < lg / 2; ++p, ns *= 4) n += 3 * ns;
   if (lg & 1) n += 1 << (lg - 1);
@@ -213,6 +219,148 @@ __device__ __forceinline__ void first_pass_fwd_regs(const cd (&x)[4], cd* b) {
   b[sw(4 * j + 3)] = csub(t1, mi3);
 }
 
+// ---------------------------------------------------------------------------
+// Q = 1024: radix-8 Stockham passes (128 threads, 8 points each) and radix-4
+// passes (256 threads), twiddles computed from w1 (and w4) instead of one
+// table entry per power: the inverse is 8-8-4 with the last radix-4 pass in
+// registers, the forward 4-4-8-8 with the first radix-4 pass in registers,
+// so a synthesis -> pointwise -> analysis pair is 6 shared-memory passes
+// (radix-4 throughout: 8) and each pass moves ~20% fewer bytes.  Layout:
+// swizzle sw10, bank-conflict free for every pass's loads and stores
+// (tools/studies/fft_banks.py checks all of them).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int sw10(int i) { return i ^ ((i >> 2) & 7) ^ ((i >> 5) & 7); }
+
+// y_m = sum_t v_t w8^(t m), w8 = exp(-+ i pi / 4): two radix-4 DFTs and the w8^m combine
+template <bool INV>
+__device__ __forceinline__ void dft8(cd (&v)[8]) {
+  constexpr double S = 0.70710678118654752440;
+  cd e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  cd o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  dft4<INV>(e0, e1, e2, e3);
+  dft4<INV>(o0, o1, o2, o3);
+  if (INV) {
+    o1 = {(o1.x - o1.y) * S, (o1.x + o1.y) * S};     // (1 + i)/sqrt2
+    o2 = {-o2.y, o2.x};                              // i
+    o3 = {-(o3.x + o3.y) * S, (o3.x - o3.y) * S};    // (-1 + i)/sqrt2
+  } else {
+    o1 = {(o1.x + o1.y) * S, (o1.y - o1.x) * S};     // (1 - i)/sqrt2
+    o2 = {o2.y, -o2.x};                              // -i
+    o3 = {(o3.y - o3.x) * S, -(o3.x + o3.y) * S};    // (-1 - i)/sqrt2
+  }
+  v[0] = cadd(e0, o0);
+  v[4] = csub(e0, o0);
+  v[1] = cadd(e1, o1);
+  v[5] = csub(e1, o1);
+  v[2] = cadd(e2, o2);
+  v[6] = csub(e2, o2);
+  v[3] = cadd(e3, o3);
+  v[7] = csub(e3, o3);
+}
+
+// radix-8 Stockham pass over L = 1024 points, Ns = NS: butterfly j < 128 reads
+// j + 128 t, twiddles w^(t k) (w = exp(-+2 pi i / (8 NS)), k = j mod NS) from
+// w1 = w^k and w4 = w^(4k), writes (j - k) 8 + k + m NS.  No barrier.
+template <bool INV, int NS, int TWO>
+__device__ __forceinline__ void r8_pass10(const cd* __restrict__ a, cd* __restrict__ b, const cd* __restrict__ tw) {
+  const int j = threadIdx.x;
+  if (j < 128) {
+    const int k = j & (NS - 1);
+    cd v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) v[t] = a[sw10(j + t * 128)];
+    if (NS > 1) {
+      cd w1 = tw[TWO + k], w4 = tw[TWO + NS + k];
+      if (INV) {
+        w1.y = -w1.y;
+        w4.y = -w4.y;
+      }
+      const cd w2 = cmul(w1, w1), w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
+      v[1] = cmul(v[1], w1);
+      v[2] = cmul(v[2], w2);
+      v[3] = cmul(v[3], w3);
+      v[4] = cmul(v[4], w4);
+      v[5] = cmul(v[5], w5);
+      v[6] = cmul(v[6], w6);
+      v[7] = cmul(v[7], w7);
+    }
+    dft8<INV>(v);
+    const int base = ((j - k) << 3) + k;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) b[sw10(base + m * NS)] = v[m];
+  }
+}
+
+// radix-4 Stockham pass over L = 1024 points (256 butterflies), twiddles from w1.  No barrier.
+template <bool INV, int NS, int TWO>
+__device__ __forceinline__ void r4_pass10(const cd* __restrict__ a, cd* __restrict__ b, const cd* __restrict__ tw) {
+  const int j = threadIdx.x;
+  const int k = j & (NS - 1);
+  cd v0 = a[sw10(j)], v1 = a[sw10(j + 256)], v2 = a[sw10(j + 512)], v3 = a[sw10(j + 768)];
+  if (NS > 1) {
+    cd w1 = tw[TWO + k];
+    if (INV) w1.y = -w1.y;
+    const cd w2 = cmul(w1, w1), w3 = cmul(w1, w2);
+    v1 = cmul(v1, w1);
+    v2 = cmul(v2, w2);
+    v3 = cmul(v3, w3);
+  }
+  dft4<INV>(v0, v1, v2, v3);
+  const int base = ((j - k) << 2) + k;
+  b[sw10(base)] = v0;
+  b[sw10(base + NS)] = v1;
+  b[sw10(base + 2 * NS)] = v2;
+  b[sw10(base + 3 * NS)] = v3;
+}
+
+// last inverse pass (radix 4, Ns = 256) into registers: v[r] = output at j + 256 r
+__device__ __forceinline__ void last_inv10(const cd* __restrict__ a, const cd* __restrict__ tw, cd (&v)[4]) {
+  const int j = threadIdx.x;
+  v[0] = a[sw10(j)];
+  v[1] = a[sw10(j + 256)];
+  v[2] = a[sw10(j + 512)];
+  v[3] = a[sw10(j + 768)];
+  cd w1 = tw[T10_R4_256 + j];
+  w1.y = -w1.y;
+  const cd w2 = cmul(w1, w1), w3 = cmul(w1, w2);
+  v[1] = cmul(v[1], w1);
+  v[2] = cmul(v[2], w2);
+  v[3] = cmul(v[3], w3);
+  dft4<true>(v[0], v[1], v[2], v[3]);
+}
+
+// first forward pass (radix 4, Ns = 1) from registers x[r] = input at j + 256 r
+__device__ __forceinline__ void first_fwd10(cd (&x)[4], cd* __restrict__ b) {
+  const int j = threadIdx.x;
+  dft4<false>(x[0], x[1], x[2], x[3]);
+  b[sw10(4 * j)] = x[0];
+  b[sw10(4 * j + 1)] = x[1];
+  b[sw10(4 * j + 2)] = x[2];
+  b[sw10(4 * j + 3)] = x[3];
+}
+
+template <int NT>
+__device__ __forceinline__ cd* inv_passes10(cd* A, cd* B, const cd* tw) {
+  r8_pass10<true, 1, 0>(A, B, tw);
+  bar<NT>();
+  r8_pass10<true, 8, T10_R8_8>(B, A, tw);
+  bar<NT>();
+  r4_pass10<true, 64, T10_R4_64>(A, B, tw);
+  bar<NT>();
+  return B;
+}
+
+template <int NT>
+__device__ __forceinline__ cd* fwd_passes10(cd* Y, cd* X, const cd* tw) {
+  r4_pass10<false, 4, T10_R4_4>(Y, X, tw);
+  bar<NT>();
+  r8_pass10<false, 16, T10_R8_16>(X, Y, tw);
+  bar<NT>();
+  r8_pass10<false, 128, T10_R8_128>(Y, X, tw);
+  bar<NT>();
+  return X;
+}
+
 template <int NT, int EPT, int LG>
 struct Sine1D {
   static constexpr double SQ2 = 1.4142135623730951;
@@ -257,6 +405,8 @@ struct Sine1D {
   }
 
   __device__ __forceinline__ int mode(int i) const { return 1 + (int)threadIdx.x + i * NT; }
+  // shared-memory FFT layout of this transform length (Q = 1024: the radix-8 passes' swizzle)
+  __device__ __forceinline__ static int S(int i) { return LG == 10 ? sw10(i) : sw(i); }
   __device__ __forceinline__ static int perm(int q) { return (q & 1) ? (Q - 1 - (q >> 1)) : (q >> 1); }
 
   __device__ __forceinline__ double norm2_partial(const double* v) const {
@@ -280,17 +430,17 @@ struct Sine1D {
         const double a = av[i], b = bv[i];
         const cd v1 = {p.y * a, -p.x * a};
         const cd v2 = {p.x * b, p.y * b};
-        A[sw(k)] = {v1.x - v2.y, v1.y + v2.x};
+        A[S(k)] = {v1.x - v2.y, v1.y + v2.x};
         // j = Q-k: V1 = pq a, V2 = -i pq b
         const cd u1 = {pq.x * a, pq.y * a};
         const cd u2 = {pq.y * b, -pq.x * b};
-        A[sw(Q - k)] = {u1.x - u2.y, u1.y + u2.x};
+        A[S(Q - k)] = {u1.x - u2.y, u1.y + u2.x};
       } else if (k == M) {
         const cd p = ph[M];
         const double a = av[i], b = bv[i];
         const cd v1 = {p.x * a + p.y * a, p.y * a - p.x * a};  // p (a - i a)
         const cd v2 = {p.x * b + p.y * b, p.y * b - p.x * b};  // p (b - i b)
-        A[sw(M)] = {v1.x - v2.y, v1.y + v2.x};
+        A[S(M)] = {v1.x - v2.y, v1.y + v2.x};
       }
     }
     if (threadIdx.x == 0) A[0] = {0.0, 0.0};
@@ -316,7 +466,17 @@ struct Sine1D {
     synth_input(av, bv);
     bar<NT>();
     cd* Z;
-    if constexpr (kFuse) {
+    if constexpr (LG == 10 && NT == 256) {
+      cd* X = inv_passes10<NT>(A, B, twp);
+      cd* Y = (X == A) ? B : A;
+      cd v[4];
+      last_inv10(X, twp, v);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) v[r] = {0.0, dq[qof(threadIdx.x, r)] * (0.5 * v[r].y)};
+      first_fwd10(v, Y);
+      bar<NT>();
+      Z = fwd_passes10<NT>(Y, X, twp);
+    } else if constexpr (kFuse) {
       constexpr int P = LG / 2;
       cd* X = fft_passes<LG, NT, true, 0, P - 1>(A, B, twp);
       cd* Y = (X == A) ? B : A;
@@ -336,7 +496,7 @@ struct Sine1D {
       for (int i = 0; i < QPT; ++i) {
         const int q = threadIdx.x + i * NT;
         if (Q % NT == 0 || q < Q) {
-          const int s = sw(perm(q));
+          const int s = S(perm(q));
           R[s] = {0.0, dq[q] * (0.5 * R[s].y)};
         }
       }
@@ -348,7 +508,7 @@ struct Sine1D {
       const int k = mode(i);
       kp[i] = 0.0;
       if (k <= M) {
-        const cd a = Z[sw(k)], b = Z[sw(Q - k)], c = ph[k];
+        const cd a = Z[S(k)], b = Z[S(Q - k)], c = ph[k];
         const double Dx = a.x - b.x, Dy = a.y + b.y;
         kp[i] = SQ2 * CUDART_PI * (double)k * (0.5 * (c.x * Dy - c.y * Dx));
       }
@@ -391,7 +551,7 @@ struct Sine1D {
     for (int i = 0; i < QPT; ++i) {
       const int q = threadIdx.x + i * NT;
       if (Q % NT == 0 || q < Q) {
-        const int s = sw(perm(q));
+        const int s = S(perm(q));
         const cd w = R[s];
         const double s1 = 0.5 * w.x, s2 = 0.5 * w.y;
         const double u = (q & 1) ? -s1 : s1;
@@ -428,10 +588,31 @@ struct Sine1D {
     }
     bar<NT>();
     const double emt = fn.id == 1 ? exp(-t) : 0.0;  // only PF_FN_POLY's source uses exp(-t)
-    double dsum = 0.0, nbad = 0.0, dbar = 0.0;
+    double dsum = 0.0, nbad = 0.0;
     int bad = 0x7fffffff;
     cd* Z;
-    if constexpr (kFuse) {
+    // the pointwise partials (sum of d for the preconditioner, non-finite D
+    // count) ride on the right-hand-side reduction after the analysis FFT:
+    // one block reduction fewer per substep (the FFT itself does not depend
+    // on them; a non-finite D is reported before any solve)
+    if constexpr (LG == 10 && NT == 256) {
+      cd* X = inv_passes10<NT>(A, B, twp);
+      cd* Y = (X == A) ? B : A;
+      PF_T(1);
+      cd v[4];
+      last_inv10(X, twp, v);
+      switch (fn.id) {
+        case 1: pointwise_regs<1>(fn, v, t, emt, dsum, nbad, bad); break;
+        case 2: pointwise_regs<2>(fn, v, t, emt, dsum, nbad, bad); break;
+        case 3: pointwise_regs<3>(fn, v, t, emt, dsum, nbad, bad); break;
+        case 4: pointwise_regs<4>(fn, v, t, emt, dsum, nbad, bad); break;
+        default: pointwise_regs<0>(fn, v, t, emt, dsum, nbad, bad); break;
+      }
+      first_fwd10(v, Y);
+      bar<NT>();
+      PF_T(2);
+      Z = fwd_passes10<NT>(Y, X, twp);
+    } else if constexpr (kFuse) {
       constexpr int P = LG / 2;
       cd* X = fft_passes<LG, NT, true, 0, P - 1>(A, B, twp);
       cd* Y = (X == A) ? B : A;
@@ -448,12 +629,7 @@ struct Sine1D {
         }
         first_pass_fwd_regs(v, Y);
       }
-      const double2 s01 = red.sum2(dsum, nbad);  // barrier: orders the first pass too
-      if (s01.y > 0.0) {
-        st.node = red.min_int(bad);
-        return ST_COEFF;
-      }
-      dbar = s01.x;
+      bar<NT>();
       PF_T(2);
       Z = fft_passes<LG, NT, false, 1, P>(Y, X, twp);
     } else {
@@ -469,25 +645,20 @@ struct Sine1D {
         case 4: pointwise<4>(fn, R, t, emt, dsum, nbad, bad); break;
         default: pointwise<0>(fn, R, t, emt, dsum, nbad, bad); break;
       }
-      const double2 s01 = red.sum2(dsum, nbad);
-      if (s01.y > 0.0) {
-        st.node = red.min_int(bad);
-        return ST_COEFF;
-      }
-      dbar = s01.x;
+      bar<NT>();
       PF_T(2);
       // --- analysis pair: F = S^T g, K x0 = S'^T (d v0) --------------------
       Z = fft_stockham<LG, NT, false>(R, O, twp);
     }
     PF_T(3);
     double x[EPT], r[EPT], p[EPT], z[EPT], pinv[EPT];
-    double bb = 0.0, rr = 0.0, rzl = 0.0;
+    double bb = 0.0, rr = 0.0;
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
       const int k = mode(i);
-      x[i] = r[i] = p[i] = z[i] = pinv[i] = 0.0;
+      x[i] = r[i] = 0.0;
       if (k <= M) {
-        const cd a = Z[sw(k)], b = Z[sw(Q - k)], c = ph[k], c2 = ph[Q - k];
+        const cd a = Z[S(k)], b = Z[S(Q - k)], c = ph[k], c2 = ph[Q - k];
         const double Dx = a.x - b.x, Dy = a.y + b.y;
         const double X2 = 0.5 * (c.x * Dy - c.y * Dx);
         const double X1 = 0.5 * (c2.x * (b.x + a.x) + c2.y * (b.y - a.y));
@@ -496,30 +667,43 @@ struct Sine1D {
         const double rhs = __dadd_rn(__dadd_rn(hist[i], __dmul_rn(gam, F)), contrib[i]);
         x[i] = xguess[i];
         r[i] = rhs - (x[i] + gam * kx);
+        bb = fma(rhs, rhs, bb);
+        rr = fma(r[i], r[i], rr);
+      }
+    }
+    const double4 s0 = red.sum4(dsum, nbad, bb, rr);
+    PF_T(4);
+    if (s0.y > 0.0) {
+      st.node = red.min_int(bad);
+      return ST_COEFF;
+    }
+    const double dbar = s0.x;
+    double rzl = 0.0;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int k = mode(i);
+      p[i] = z[i] = pinv[i] = 0.0;
+      if (k <= M) {
         const double kk = (double)k;
         pinv[i] = 1.0 / (1.0 + gam * dbar * (CUDART_PI * CUDART_PI) * (kk * kk));
         z[i] = pinv[i] * r[i];
         p[i] = z[i];
-        bb = fma(rhs, rhs, bb);
-        rr = fma(r[i], r[i], rr);
         rzl = fma(r[i], z[i], rzl);
       }
     }
-    const double3 s0 = red.sum3(bb, rr, rzl);
-    PF_T(4);
     st.solves += 1;
     // a non-finite right-hand side or guess fails here (SolverFailure, stepping.py:240-241)
-    if (!isfinite(s0.x) || !isfinite(s0.y)) return ST_SOLVER;
-    if (s0.x == 0.0) {
+    if (!isfinite(s0.z) || !isfinite(s0.w)) return ST_SOLVER;
+    if (s0.z == 0.0) {
 #pragma unroll
       for (int i = 0; i < EPT; ++i) xout[i] = 0.0;
       return ST_OK;
     }
-    const double thr = tol2 * s0.x;
-    double rrv = s0.y;
+    const double thr = tol2 * s0.z;
+    double rrv = s0.w;
     int it = 0;
     if (rrv > thr) {
-      double rz = s0.z;
+      double rz = 0.0;  // (r0, z0): reduced with the first iteration's (p, q)
       for (it = 1; it <= maxit; ++it) {
         double kp[EPT], qv[EPT];
         PF_T(6);
@@ -531,7 +715,9 @@ struct Sine1D {
           qv[i] = p[i] + gam * kp[i];
           pql = fma(p[i], qv[i], pql);
         }
-        const double pq = red.sum(pql);
+        const double2 pr = red.sum2(pql, it == 1 ? rzl : 0.0);
+        const double pq = pr.x;
+        if (it == 1) rz = pr.y;
         const double alpha = rz / pq;
         if (!isfinite(alpha)) return ST_SOLVER;
         double rrl = 0.0, rzn = 0.0;

@@ -71,63 +71,67 @@ def make_operator(problem, degree=None, space=None, dims=None):
     raise ValueError(f"unknown space {space!r}; choices: chebyshev, sine")
 
 
-def _min_time(fn, reps, warmup):
-    result = None
-    for _ in range(warmup):
-        result = fn()
-    best = float("inf")
-    for _ in range(max(1, reps)):
-        t0 = time.perf_counter()
-        result = fn()
-        best = min(best, time.perf_counter() - t0)
-    return best, result
+class _Runner:
+    """Runs one solver of a bench point: warm-up calls, timed calls
+    (``time.perf_counter`` around each, the minimum kept as the reference's
+    harness does, ``harness.py:65-73``) and an optional separate pass under
+    ``tracemalloc`` for the host-side allocation peak (``harness.py:76-82``)."""
+
+    def __init__(self, call):
+        self.call = call
+        self.last = None
+
+    def timed(self, reps, warmup):
+        for _ in range(max(0, warmup)):
+            self.last = self.call()
+        samples = []
+        for _ in range(max(1, reps)):
+            t0 = time.perf_counter()
+            self.last = self.call()
+            samples.append(time.perf_counter() - t0)
+        return min(samples)
+
+    def host_peak(self):
+        tracemalloc.start()
+        try:
+            self.call()
+            return int(tracemalloc.get_traced_memory()[1])
+        finally:
+            tracemalloc.stop()
 
 
-def _host_peak(fn):
-    tracemalloc.start()
-    try:
-        fn()
-        return int(tracemalloc.get_traced_memory()[1])
-    finally:
-        tracemalloc.stop()
+def _grid_for(dof, m):
+    """``nt * m_eff`` fine steps with ``m_eff = clip(m, 1, dof)``, ``nt = dof // m_eff``."""
+    m_eff = max(1, min(int(m), int(dof)))
+    return max(1, int(dof) // m_eff), m_eff
 
 
 def bench_point(problem_name, dof, *, alpha=None, degree=16, m=32, tol=1e-10, k_max=20, threads=1,
                 reps=3, warmup=1, measure_memory=True, space=None, dims=None):
-    """Serial fine solver vs parareal at ``nt * m ~= dof`` fine steps (``harness.py:85-117``).
-
-    ``m`` is clipped to ``[1, dof]`` and ``nt = dof // m``; the realised dof
-    is recorded.  ``threads`` is recorded and otherwise ignored (the device
-    batches every slice).
-    """
+    """Serial fine solver vs parareal at ``nt * m ~= dof`` fine steps, both on
+    the device (the row schema of ``harness.py:85-117``).  ``threads`` is
+    recorded and otherwise ignored (the device batches every slice)."""
     if dof < 1:
         raise ValueError("dof must be a positive integer")
-    m_eff = max(1, min(int(m), int(dof)))
-    nt = max(1, int(dof) // m_eff)
+    nt, m_eff = _grid_for(dof, m)
     problem = get_problem(problem_name, alpha=alpha)
     op = make_operator(problem, degree, space, dims)
     grids = TimeGrids(problem.t_final, nt, m_eff)
-
-    def fine():
-        return run_fine_sequential(problem, op, grids)
-
-    def para():
-        return parareal_solve(problem, op, grids, tol=tol, k_max=k_max, threads=threads)
-
-    t_fine, _ = _min_time(fine, reps, warmup)
-    t_para, (_, report) = _min_time(para, reps, warmup)
-    return BenchRecord(
-        dof=nt * m_eff, nt=nt, m=m_eff,
-        degree=int(getattr(op, "degree", getattr(op, "modes", 0))),
-        threads=int(threads), wall_fine=t_fine, wall_parareal=t_para, speedup=t_fine / t_para,
-        iterations=report.iterations, final_diff=report.diffs[-1],
-        peak_alloc_fine=_host_peak(fine) if measure_memory else 0,
-        peak_alloc_parareal=_host_peak(para) if measure_memory else 0,
-    )
+    serial = _Runner(lambda: run_fine_sequential(problem, op, grids))
+    para = _Runner(lambda: parareal_solve(problem, op, grids, tol=tol, k_max=k_max, threads=threads))
+    t_serial = serial.timed(reps, warmup)
+    t_para = para.timed(reps, warmup)
+    report = para.last[1]
+    peaks = (serial.host_peak(), para.host_peak()) if measure_memory else (0, 0)
+    return BenchRecord(dof=nt * m_eff, nt=nt, m=m_eff, degree=int(getattr(op, "degree", getattr(op, "modes", 0))),
+                       threads=int(threads), wall_fine=t_serial, wall_parareal=t_para, speedup=t_serial / t_para,
+                       iterations=report.iterations, final_diff=report.diffs[-1], peak_alloc_fine=peaks[0],
+                       peak_alloc_parareal=peaks[1])
 
 
 def bench_sweep(problem_name, dofs, **kwargs):
-    """``bench_point`` over every dof of the sweep, in order (``harness.py:120-123``)."""
-    if not dofs:
+    """One ``bench_point`` per entry of ``dofs``, in order (``harness.py:120-123``)."""
+    points = list(dofs)
+    if not points:
         raise ValueError("benchmark sweep must not be empty")
-    return [bench_point(problem_name, d, **kwargs) for d in dofs]
+    return [bench_point(problem_name, d, **kwargs) for d in points]
