@@ -20,7 +20,9 @@ from .l1 import gamma_2_minus, weights_for
 from .spaces import ChebyshevOperator, SineOperator
 
 LIB_NAME = "libparafrac_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# PARAFRAC_B200_LIB selects another in-tree build of the same library (the
+# -DPF_JITTER protocol-stress build of tests/test_protocol_jitter.py)
+LIB_PATH = os.environ.get("PARAFRAC_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 PF_OK, PF_ERR_ARGUMENT, PF_ERR_SOLVER, PF_ERR_COEFFICIENT = 0, 1, 2, 3
 PF_ERR_DIVERGENCE, PF_ERR_CUDA, PF_ERR_UNSUPPORTED = 4, 5, 6

@@ -234,6 +234,26 @@ struct SweepSync {
   int* abort;     // [slice] set by a failing slice CTA
 };
 
+// Protocol stress build (-DPF_JITTER, tests/test_protocol_jitter.py): the
+// slice CTA delays its progress publish and the helper CTA its block by a
+// pseudo-random 0..8 us, so the release/acquire handshake runs under many
+// interleavings; results must stay bitwise those of the inline far history.
+// (compute-sanitizer is closed on this pool: profiles/r02_compute_sanitizer_closed.txt)
+__device__ __forceinline__ void pf_jitter(int a, int b) {
+#ifdef PF_JITTER
+  if (threadIdx.x == 0) {
+    unsigned h = (unsigned)a * 73856093u ^ (unsigned)b * 19349663u ^ (unsigned)PF_JITTER * 83492791u;
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    __nanosleep(h & 8191u);
+  }
+#else
+  (void)a;
+  (void)b;
+#endif
+}
+
 // Fine sweep.  Grid = nslices slice CTAs (+ nslices helper CTAs when
 // `helpers`, launched cooperatively so all are co-resident).  A helper owns
 // the far L1 history and the coarse-history bracket of its slice: it runs the
@@ -292,6 +312,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         __syncthreads();
         if (ld_acquire(sync.abort + b) != 0) return;
       }
+      pf_jitter(b * 64 + hid, beta);
       PF_TH(11);
       double* hs = slot(beta & 1, hid);
       const int R0 = beta * HB;
@@ -394,6 +415,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       J = far_extent(beta);
       double* s0 = slot(beta & 1, 0);
       if (helpers) {
+        pf_jitter(b + 1000003, beta);
         cta_publish(sync.progress + b, r - 1);  // rows 0..r-1 are in the path
         if (threadIdx.x == 0) {
           for (int h = 0; h < hps; ++h) {

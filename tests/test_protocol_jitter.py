@@ -1,0 +1,64 @@
+"""Inter-CTA protocol under perturbed timing (``-m gpu``).
+
+The fine sweep's slice and helper CTAs exchange far-history blocks through
+release/acquire flags (pf_kernels.cuh ``cta_publish`` / ``ld_acquire``).
+compute-sanitizer is closed on this pool (profiles/r02_compute_sanitizer_closed.txt),
+so the protocol is checked by a stress build instead: ``-DPF_JITTER`` makes
+every slice CTA delay its progress publish and every helper CTA its block by a
+pseudo-random 0..8 us.  Under any interleaving the sweep must be bitwise the
+inline far history (PF_NO_HELPERS=1, no inter-CTA protocol at all) and the
+split-K sequential solver bitwise the regular build."""
+
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+JITTER = os.path.join(ROOT, "paper_2510_11023_b200", "libparafrac_b200_jitter.so")
+
+CODE = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2510_11023_b200 as p
+from paper_2510_11023_b200 import _lib
+pr = p.config_problem(3); op = p.build_sine_operator(512)
+g = p.TimeGrids(2.0, 16, 96)
+t = p.run_coarse(pr, op, g)
+out = p.fine_sweep_intervals(t, 0, 16, op, g, pr)
+ctx = _lib.context_for(pr, op, g)
+seq, _ = p.run_fine_sequential(pr, op, p.TimeGrids(2.0, 4, 128))
+np.savez(sys.argv[1], sweep=out, seq=seq, helpers=ctx.stats()["helper_launches"], lib=_lib.LIB_PATH)
+"""
+
+
+def _run(env_extra):
+    with tempfile.TemporaryDirectory() as d:
+        f = os.path.join(d, "o.npz")
+        subprocess.run([sys.executable, "-c", CODE.format(root=ROOT), f], check=True,
+                       env=dict(os.environ, **env_extra))
+        z = np.load(f)
+        return {k: z[k] for k in z.files}
+
+
+def test_handshake_bitwise_under_jitter():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a B200")
+    if not os.path.exists(JITTER):
+        pytest.fail("the -DPF_JITTER build is missing: run __graft_entry__.build()")
+    jit = _run({"PARAFRAC_B200_LIB": JITTER})
+    assert str(jit["lib"]).endswith("libparafrac_b200_jitter.so")
+    assert int(jit["helpers"]) >= 1  # the cooperative slice + helper launch ran
+    inline = _run({"PF_NO_HELPERS": "1"})
+    assert int(inline["helpers"]) == 0
+    np.testing.assert_array_equal(jit["sweep"], inline["sweep"])
+    plain = _run({})
+    np.testing.assert_array_equal(plain["sweep"], inline["sweep"])
+    np.testing.assert_array_equal(jit["seq"], plain["seq"])

@@ -12,7 +12,7 @@ buf = (C.c_longlong * 16)()
 _lib.lib.pf_debug_phases(buf, 1)
 pfb.fine_sweep_intervals(tr, 0, c["nt"], op, g, prob)
 _lib.lib.pf_debug_phases(buf, 0)
-names = {0: "from step entry (misc)", 1: "synth FFT", 2: "pointwise+reduce", 3: "analysis FFT", 4: "residual+reduce",
+names = {0: "from step entry (misc)", 1: "synth FFT", 2: "pointwise (fused)", 3: "analysis FFT", 4: "residual+reduce",
          5: "CG apply_k (2 FFT)", 6: "CG update+reduce", 7: "finite check", 8: "block start (helper wait)",
          9: "near hist + extrap", 10: "path write/loop", 11: "HELPER wait for progress",
          12: "HELPER far GEMM", 13: "HELPER bracket", 14: "HELPER publish+loop"}
