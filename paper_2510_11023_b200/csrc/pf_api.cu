@@ -99,7 +99,8 @@ struct pf_ctx {
   int num_sms = 0;
   int allow_helpers = 1;  // PF_NO_HELPERS=1 forces the inline far history
   int last_helpers = 0;
-  Engine2D* e2 = nullptr;  // PF_SPACE_SINE2D only
+  Engine2D* e2 = nullptr;   // PF_SPACE_SINE2D only
+  Engine2D* e2c = nullptr;  // batch-1 engine of the graph-captured sequential sweeps (stable buffers)
 };
 
 namespace {  // 2-D engine entry points (defined in pf_engine2d.inc)
@@ -707,6 +708,7 @@ void pf_destroy(pf_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c->e2;
+  delete c->e2c;
   delete c;
 }
 

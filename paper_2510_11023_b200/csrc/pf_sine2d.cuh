@@ -1257,4 +1257,48 @@ __global__ void k2_node_norms(const double* unext, const double* ucur, long MM, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident sequential sweeps (pf_engine2d.inc e2_graph_*): the batch-1
+// coarse solves of run_coarse and of the parareal correction sweep run as one
+// CUDA graph per sweep, the PCG loop of each solve a conditional WHILE node and
+// the frozen-prefix test (the solve is skipped while U_next[0..n] == U_cur[0..n]
+// bitwise) a conditional IF node -- no host round trip per iteration or node.
+// ---------------------------------------------------------------------------
+
+// frozen-prefix test of node n: while *same, compare U_next[n] with U_cur[n]
+// (node 0 is never compared: U_next[0] = U_cur[0]); *differs is zero on entry
+__global__ void k2_differs_gated(const double* a, const double* b, long MM, int n, const int* same, int* differs) {
+  if (n == 0 || *same == 0) return;
+  int d = 0;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < (size_t)MM; e += (size_t)gridDim.x * blockDim.x)
+    d |= __double_as_longlong(a[e]) != __double_as_longlong(b[e]);
+  if (__syncthreads_or(d) && threadIdx.x == 0) *differs = 1;
+}
+
+// same := same && !differs; the IF node solves node n unless the prefix is still frozen
+__global__ void k2_cond_solve(int* same, const int* differs, cudaGraphConditionalHandle h) {
+  if (*same != 0 && *differs != 0) *same = 0;
+  cudaGraphSetConditional(h, *same != 0 ? 0u : 1u);
+}
+
+// WHILE condition of a PCG loop: systems left unconverged by the last update
+__global__ void k2_cond_while(cudaGraphConditionalHandle h, const int* remaining) {
+  cudaGraphSetConditional(h, *remaining > 0 ? 1u : 0u);
+}
+
+// per-node outcome of a batch-1 solve: {solved, PCG iterations, failure kind, bad node}
+__global__ void k2_node_status(Sine2DArgs a, int n, int4* st) {
+  st[n] = make_int4(1, (int)a.sc[S_IT], (int)a.sc[S_FAIL], a.bad[0]);
+}
+
+// U_next[n+1] = F_old[n] + (G_new[n] - G_old[n]); a frozen node takes G_new[n] = G_old[n]
+__global__ void k2_correct_row_gated(const double* fold, double* gnew, const double* gold, double* unext, long MM,
+                                     const int* same) {
+  const bool frozen = *same != 0;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < (size_t)MM; e += (size_t)gridDim.x * blockDim.x) {
+    if (frozen) gnew[e] = gold[e];
+    unext[e] = fold[e] + (gnew[e] - gold[e]);
+  }
+}
+
 }  // namespace pf
