@@ -1281,10 +1281,6 @@ __global__ void k2_cond_solve(int* same, const int* differs, cudaGraphConditiona
   cudaGraphSetConditional(h, *same != 0 ? 0u : 1u);
 }
 
-__global__ void k2_update_same(int* same, const int* differs) {
-  if (*same != 0 && *differs != 0) *same = 0;
-}
-
 // small integer fills inside graph bodies (memset nodes in device-launched
 // conditional bodies cost far more than a one-thread kernel)
 __global__ void k2_fill_int(int* p, int v) { *p = v; }
