@@ -80,7 +80,7 @@ def main():
     nt = a.nt or nt
     m = a.m or m
     k_max = a.kmax or nt + 1
-    stride = a.stride or max(1, nt // 32)
+    stride = a.stride or max(1, nt // 8)
     _init(i, M, nt, m, T)
     space, grids, prob = _W["space"], _W["grids"], _W["prob"]
     t0 = time.time()
