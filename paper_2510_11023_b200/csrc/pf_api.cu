@@ -241,9 +241,13 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   const int m = m_override > 0 ? m_override : c->grid.m;
   const int hps = std::max(1, hps_req);
   if (c->paths.ensure((size_t)bs * (m + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "paths");
-  if (c->scratch.ensure((size_t)bs * 2 * (hps + 1) * 2 * pf::HB * c->size))
-    return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
-  const int nsync = bs * (2 + hps);
+  // per slice: block tiles [parity][hps + 1][2][HB][size] (+ the split tensor-core
+  // helpers' part tiles [parity][batch][part][512], k_fine_sweep)
+  const bool tc = c->kind == PF_SPACE_SINE1D && c->lgQ >= 10 && c->size % pf::TC_BATCH == 0;
+  const size_t parts_len = (tc && hps > 1) ? (size_t)2 * (c->size / pf::TC_BATCH) * 8 * 512 : 0;
+  const size_t scr_stride = (size_t)2 * (hps + 1) * 2 * pf::HB * c->size + parts_len;
+  if (c->scratch.ensure((size_t)bs * scr_stride)) return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
+  const int nsync = bs * (2 + hps) + bs * 64;
   if (c->sync_cap < nsync) {
     if (c->d_sync) cudaFree(c->d_sync);
     c->d_sync = nullptr;
@@ -257,14 +261,14 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   cm.x_start = d_start;
   PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
   if (bs > 65535) return set_error(c, PF_ERR_UNSUPPORTED, "more than 65535 slices in one sweep launch");
-  const size_t scr_stride = (size_t)2 * (hps + 1) * 2 * pf::HB * c->size;  // per-slice scratch (k_fine_sweep)
   // Launch the sweep of slices [n_lo + s0, n_lo + s0 + ns) (local slices s0..) on stream st:
   // per-slice sync flags, paths, scratch, outputs and status at the local offsets.
   auto sweep = [&](int s0, int ns, cudaStream_t st, const double* brk) -> int {
     pf::Common cl = cm;
     cl.scratch = c->scratch.p + (size_t)s0 * scr_stride;
     cl.brk = brk;
-    pf::SweepSync sync{c->d_sync + s0, c->d_sync + bs + (size_t)s0 * hps, c->d_sync + bs + (size_t)bs * hps + s0};
+    pf::SweepSync sync{c->d_sync + s0, c->d_sync + bs + (size_t)s0 * hps, c->d_sync + bs + (size_t)bs * hps + s0,
+                       c->d_sync + 2 * bs + (size_t)bs * hps + (size_t)s0 * 64};
     double* dp = c->paths.p + (size_t)s0 * (m + 1) * c->size;
     double* dout = d_out ? d_out + (size_t)s0 * c->size : nullptr;
     Status* dst = d_st + s0;
@@ -275,11 +279,16 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
       // shared-memory ring of the last NR states behind the space's own smem
       const size_t ring_bytes = sizeof(double) * pf::NR * c->size;
       const size_t base = (c->smem + 15) & ~size_t(15);
-      int ring_off = -1;
+      int ring_off = -1, red_off = -1;
       size_t smem = c->smem;
       if (base + ring_bytes <= 227 * 1024) {
         ring_off = (int)base;
         smem = base + ring_bytes;
+      }
+      // the tensor-core far history's part buffer (inline path; helpers reuse the space)
+      if (tc && smem + sizeof(double) * pf::TC_RED <= 227 * 1024) {
+        red_off = (int)smem;
+        smem += sizeof(double) * pf::TC_RED;
       }
       PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       PF_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
@@ -289,10 +298,11 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
       int smem_total = (int)smem;
       if (helpers) {
         void* args[] = {(void*)&cl, (void*)&spp, (void*)&d_u, (void*)&nl, (void*)&nsl, (void*)&helpers,
-                        (void*)&ring_off, (void*)&smem_total, (void*)&sync, (void*)&dp, (void*)&dout, (void*)&dst};
+                        (void*)&ring_off, (void*)&smem_total, (void*)&red_off, (void*)&sync, (void*)&dp, (void*)&dout,
+                        (void*)&dst};
         PF_CUDA(c, cudaLaunchCooperativeKernel((void*)kern, dim3(ns * (1 + hps)), dim3(NT), args, smem, st));
       } else {
-        kern<<<ns, NT, smem, st>>>(cl, spp, d_u, nl, nsl, 0, ring_off, smem_total, sync, dp, dout, dst);
+        kern<<<ns, NT, smem, st>>>(cl, spp, d_u, nl, nsl, 0, ring_off, smem_total, red_off, sync, dp, dout, dst);
       }
       c->last_helpers = helpers;
     });

@@ -222,6 +222,26 @@ __device__ __forceinline__ void cta_publish(int* flag, int v) {
   __syncthreads();
   if (threadIdx.x == 0) st_release(flag, v);
 }
+// the same with a release add (counters several CTAs publish into)
+__device__ __forceinline__ void cta_publish_add(int* flag, int v) {
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+// true in the CTA that is the `count`-th to arrive on `ticket` (which it resets)
+__device__ __forceinline__ bool cta_last_arrival(int* ticket, int count) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int t = atomicAdd(ticket, 1);
+    s_last = t == count - 1;
+    if (s_last) *ticket = 0;
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  return true;
+}
 
 // History rows of block beta (target rows R0+1..R0+HB, R0 = beta*HB) folded
 // into the far part: j <= J(beta) = max(beta-1, 0)*HB.  The lag of one block
@@ -230,9 +250,104 @@ __device__ __forceinline__ int far_extent(int beta) { return (beta > 0 ? beta - 
 
 struct SweepSync {
   int* progress;  // [slice] last substep whose state row is in the path
-  int* ready;     // [slice] number of far-history blocks published
+  int* ready;     // [slice * hps + helper] far-history blocks published (tensor-core path: [slice * hps]
+                  // counts published 64-mode batches)
   int* abort;     // [slice] set by a failing slice CTA
+  int* tickets;   // [slice][parity][32] batch arrivals of the split tensor-core far history
 };
+
+// ---------------------------------------------------------------------------
+// Far history on the FP64 tensor cores: DMMA (mma.sync m8n8k4 .f64).
+// The far part of block beta is a Toeplitz GEMM
+//   out[rr][e] = b_{R0+rr} c_0[e] + sum_{j=1}^{J} a_{R0+1+rr-j} c_j[e]     (rr < HB = 8)
+// = A (8 x J, Toeplitz weights) x B (J x M, path rows): one m8n8k4 MMA per
+// k-step of 4 history rows and 8 modes, A[rr][k] = a_{R0+1+rr-(j0+k)} from
+// shared memory, B[k][n] = c_{j0+k}[8g+n] from global (L2 / HBM), the
+// accumulator C (8 target rows x 8 modes) in registers.
+// Canonical order, whoever computes it (slice CTA inline, its helper CTA, or
+// the split helpers of the sequential solver): the k-steps of a batch of 8
+// mode groups (64 modes) split into 8 interleaved parts (k-step s -> part
+// s mod 8), each accumulated in ascending s; out = b c_0 + (((P0 + P1) + ...) + P7).
+// (the sequential solver's split helpers sum sub-parts of a part first: same
+// terms, a different rounding order -- tested against the oracle, not bitwise)
+// ---------------------------------------------------------------------------
+constexpr int TC_BATCH = 64;          // modes per batch (8 groups of 8)
+constexpr int TC_RED = 8 * 8 * 64;    // doubles of the per-CTA part buffer (8 warps x 8 groups x 64)
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// One warp: the partial 8 x 64 tile of `batch` over k-steps s = s0, s0 + ds, ...
+// (rows j = 1 + 4 s + k <= J).  Lane l holds C rows l>>2, columns 2(l&3) + {0,1}
+// of each of the 8 groups.  Loads of the next k-step are in flight during the MMAs.
+__device__ __forceinline__ void tc_far_part(const double* __restrict__ path, int size, const double* __restrict__ aw,
+                                            int R0, int J, int batch, int s0, int ds, double (&acc)[8][2]) {
+  const int lane = threadIdx.x & 31, k = lane & 3, q = lane >> 2;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) acc[g][0] = acc[g][1] = 0.0;
+  const int nsteps = (J + 3) >> 2;
+  const double* col = path + TC_BATCH * batch + q;
+  double an = 0.0, bn[8];
+  auto load = [&](int st, double& av, double (&bv)[8]) {
+    const int j = 1 + 4 * st + k;
+    const bool ok = j <= J;
+    av = ok ? aw[R0 + 1 + q - j] : 0.0;
+    const double* row = col + (size_t)j * size;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) bv[g] = ok ? __ldcg(row + 8 * g) : 0.0;
+  };
+  if (s0 < nsteps) load(s0, an, bn);
+  for (int st = s0; st < nsteps; st += ds) {
+    const double ac = an;
+    double bc[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) bc[g] = bn[g];
+    if (st + ds < nsteps) load(st + ds, an, bn);
+#pragma unroll
+    for (int g = 0; g < 8; ++g) dmma884(acc[g][0], acc[g][1], ac, bc[g]);
+  }
+}
+
+// store a warp's partial tile into the CTA part buffer red[warp][g][lane][2]
+__device__ __forceinline__ void tc_store_part(double* red, const double (&acc)[8][2]) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int g = 0; g < 8; ++g)
+    reinterpret_cast<double2*>(red + ((size_t)(w * 8 + g) * 32 + lane) * 2)[0] = make_double2(acc[g][0], acc[g][1]);
+}
+
+// (rr, mode within the batch) of the 2 outputs of thread t (256 threads, 512 outputs)
+__device__ __forceinline__ void tc_out_index(int t, int i, int& slot, int& rr, int& col) {
+  slot = 2 * t + i;                        // = (g * 32 + lane) * 2 + i
+  const int g = slot >> 6, lane = (slot >> 1) & 31;
+  rr = lane >> 2;
+  col = 8 * g + 2 * (lane & 3) + i;
+}
+
+// CTA (256 threads = 8 warps): the far-history tile of `batch` in canonical order,
+// warp w accumulating part w; written to out[rr * size + 64 batch + col].
+__device__ __forceinline__ void tc_far_batch(const double* __restrict__ path, const double* __restrict__ row0,
+                                             int size, const double* __restrict__ aw, const double* __restrict__ bfine,
+                                             int R0, int J, int batch, double* red, double* out) {
+  double acc[8][2];
+  tc_far_part(path, size, aw, R0, J, batch, (int)(threadIdx.x >> 5), 8, acc);
+  tc_store_part(red, acc);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    int sl, rr, col;
+    tc_out_index((int)threadIdx.x, i, sl, rr, col);
+    const int e = TC_BATCH * batch + col;
+    double sum = red[sl];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) sum += red[(size_t)w * 512 + sl];
+    out[(size_t)rr * size + e] = bfine[R0 + rr] * __ldcg(row0 + e) + sum;
+  }
+  __syncthreads();  // red is reused by the next batch
+}
 
 // Protocol stress build (-DPF_JITTER, tests/test_protocol_jitter.py): the
 // slice CTA delays its progress publish and the helper CTA its block by a
@@ -264,7 +379,7 @@ __device__ __forceinline__ void pf_jitter(int a, int b) {
 template <class SP, class SPP, int NT, int EPT>
 __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const double* __restrict__ U, int n_lo,
                                                    int nslices, int helpers, int ring_off, int smem_total,
-                                                   SweepSync sync,
+                                                   int red_off, SweepSync sync,
                                                    double* paths,
                                                    double* __restrict__ out, Status* __restrict__ status) {
   extern __shared__ __align__(16) char smem[];
@@ -284,9 +399,86 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   const int n = n_lo + b;
   double* path = paths + (size_t)b * (c.m + 1) * c.size;
   // per slice: [parity][hps + 1][hist | bracket][HB][size]; tile hps is the combined one
-  double* scr = c.scratch + (size_t)b * 2 * (hps + 1) * 2 * HB * c.size;
+  // (+ with split tensor-core helpers: the per-batch part tiles [parity][batch][part][512])
+  const int NB = c.size / TC_BATCH;
+  const bool tc = NT == 256 && c.size % TC_BATCH == 0;  // far history on the FP64 tensor cores
+  const size_t parts_len = (tc && hps > 1) ? (size_t)2 * NB * 8 * 512 : 0;
+  double* scr = c.scratch + (size_t)b * ((size_t)2 * (hps + 1) * 2 * HB * c.size + parts_len);
   auto slot = [&](int parity, int h) { return scr + ((size_t)parity * (hps + 1) + h) * 2 * HB * c.size; };
+  double* parts = scr + (size_t)2 * (hps + 1) * 2 * HB * c.size;
   const int nblocks = (c.m + HB - 1) / HB;
+  if (helper && tc) {
+    // Toeplitz weights a_s into shared memory (when the table fits next to the part buffer)
+    const double* aw = c.afine;
+    const size_t aw_bytes = ((size_t)(c.m + HB + 1) * sizeof(double) + 15) & ~size_t(15);
+    double* red = reinterpret_cast<double*>(smem);
+    if (aw_bytes + sizeof(double) * TC_RED <= (size_t)smem_total) {
+      double* s_aw = reinterpret_cast<double*>(smem);
+      for (int q = threadIdx.x; q <= c.m + HB; q += NT) s_aw[q] = c.afine[q];
+      aw = s_aw;
+      red = reinterpret_cast<double*>(smem + aw_bytes);
+    }
+    __syncthreads();
+    __shared__ int s_abort;
+    const int w = threadIdx.x >> 5;
+    for (int beta = 0; beta < nblocks; ++beta) {
+      const int J = far_extent(beta);
+      if (J > 0) {
+        if (threadIdx.x == 0) {
+          int ns = 32;  // the slice CTA publishes a huge progress when it aborts
+          while (ld_acquire(sync.progress + b) < J) {
+            __nanosleep(ns);
+            ns = ns < 256 ? 2 * ns : ns;
+          }
+          s_abort = ld_acquire(sync.abort + b);
+        }
+        __syncthreads();
+        if (s_abort) return;
+      }
+      pf_jitter(b * 64 + hid, beta);
+      double* hs = slot(beta & 1, 0);
+      const int R0 = beta * HB;
+      const double* row0 = J > 0 ? path : (c.x_start ? c.x_start : U + (size_t)n * c.size);
+      if (hps == 1) {  // the slice's one helper: every batch, part p on warp p
+        for (int batch = 0; batch < NB; ++batch)
+          tc_far_batch(path, row0, c.size, aw, c.bfine, R0, J, batch, red, hs);
+        cta_publish_add(sync.ready + (size_t)b * hps, NB);
+      } else {  // split helpers (sequential solver): unit (batch, part) -> helper unit mod hps
+        for (int u = hid; u < NB * 8; u += hps) {
+          const int batch = u >> 3, part = u & 7;
+          double acc[8][2];
+          tc_far_part(path, c.size, aw, R0, J, batch, part + 8 * w, 64, acc);
+          tc_store_part(red, acc);
+          __syncthreads();
+          double* pb = parts + (((size_t)(beta & 1) * NB + batch) * 8 + part) * 512;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int sl = 2 * (int)threadIdx.x + i;
+            double sum = red[sl];
+#pragma unroll
+            for (int ww = 1; ww < 8; ++ww) sum += red[(size_t)ww * 512 + sl];
+            pb[sl] = sum;
+          }
+          if (cta_last_arrival(sync.tickets + (size_t)b * 64 + (beta & 1) * 32 + batch, 8)) {
+            const double* p0 = parts + ((size_t)(beta & 1) * NB + batch) * 8 * 512;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              int sl, rr, col;
+              tc_out_index((int)threadIdx.x, i, sl, rr, col);
+              const int e = TC_BATCH * batch + col;
+              double sum = __ldcg(p0 + sl);
+#pragma unroll
+              for (int pp = 1; pp < 8; ++pp) sum += __ldcg(p0 + (size_t)pp * 512 + sl);
+              hs[(size_t)rr * c.size + e] = c.bfine[R0 + rr] * __ldcg(row0 + e) + sum;
+            }
+            cta_publish_add(sync.ready + (size_t)b * hps, 1);
+          }
+          __syncthreads();  // red is reused by the next unit
+        }
+      }
+    }
+    return;
+  }
   if (helper) {
     // Toeplitz weights a_s into shared memory once (helpers own the SM's smem)
     const double* aw = c.afine;
@@ -303,14 +495,13 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         if (threadIdx.x == 0) {
           // short backoff: the slice CTA publishes once per block and every
           // microsecond of oversleep here delays the block it will wait for
-          int ns = 32;
-          while (ld_acquire(sync.progress + b) < J && ld_acquire(sync.abort + b) == 0) {
+          int ns = 32;  // the slice CTA publishes a huge progress when it aborts
+          while (ld_acquire(sync.progress + b) < J) {
             __nanosleep(ns);
             ns = ns < 256 ? 2 * ns : ns;
           }
         }
-        __syncthreads();
-        if (ld_acquire(sync.abort + b) != 0) return;
+        if (__syncthreads_or(threadIdx.x == 0 && ld_acquire(sync.abort + b) != 0)) return;
       }
       pf_jitter(b * 64 + hid, beta);
       PF_TH(11);
@@ -414,7 +605,22 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     if (rr == 0) {
       J = far_extent(beta);
       double* s0 = slot(beta & 1, 0);
-      if (helpers) {
+      if (helpers && tc) {
+        pf_jitter(b + 1000003, beta);
+        cta_publish(sync.progress + b, r - 1);  // rows 0..r-1 are in the path
+        if (threadIdx.x == 0) {  // every 64-mode batch of block beta published
+          int ns = 32;
+          while (ld_acquire(sync.ready + (size_t)b * hps) < NB * (beta + 1)) {
+            __nanosleep(ns);
+            ns = ns < 256 ? 2 * ns : ns;
+          }
+        }
+        __syncthreads();
+      } else if (tc && red_off >= 0) {
+        double* red = reinterpret_cast<double*>(smem + red_off);
+        for (int batch = 0; batch < NB; ++batch)
+          tc_far_batch(path, path, c.size, c.afine, c.bfine, beta * HB, J, batch, red, s0);
+      } else if (helpers) {
         pf_jitter(b + 1000003, beta);
         cta_publish(sync.progress + b, r - 1);  // rows 0..r-1 are in the path
         if (threadIdx.x == 0) {
@@ -540,6 +746,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     }
   } else if (helpers && threadIdx.x == 0) {
     st_release(sync.abort + b, 1);
+    st_release(sync.progress + b, 0x3fffffff);  // wakes the helpers, which then see the abort
   }
   if (threadIdx.x == 0) {
     unsigned long long tend;

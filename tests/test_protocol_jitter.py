@@ -6,8 +6,9 @@ compute-sanitizer is closed on this pool (profiles/r02_compute_sanitizer_closed.
 so the protocol is checked by a stress build instead: ``-DPF_JITTER`` makes
 every slice CTA delay its progress publish and every helper CTA its block by a
 pseudo-random 0..8 us.  Under any interleaving the sweep must be bitwise the
-inline far history (PF_NO_HELPERS=1, no inter-CTA protocol at all) and the
-split-K sequential solver bitwise the regular build."""
+inline far history (PF_NO_HELPERS=1, no inter-CTA protocol at all), and the
+sequential solver with its far history split over several helper CTAs
+(per-batch tickets, last arrival combines) bitwise the regular build."""
 
 import os
 import subprocess
@@ -33,7 +34,10 @@ t = p.run_coarse(pr, op, g)
 out = p.fine_sweep_intervals(t, 0, 16, op, g, pr)
 ctx = _lib.context_for(pr, op, g)
 seq, _ = p.run_fine_sequential(pr, op, p.TimeGrids(2.0, 4, 128))
-np.savez(sys.argv[1], sweep=out, seq=seq, helpers=ctx.stats()["helper_launches"], lib=_lib.LIB_PATH)
+g2 = p.TimeGrids(2.0, 4, 1024)  # 4096 substeps: the far history split over 4 helper CTAs
+seq2, _ = p.run_fine_sequential(pr, op, g2)
+np.savez(sys.argv[1], sweep=out, seq=seq, seq2=seq2, helpers=ctx.stats()["helper_launches"],
+         helpers2=_lib.context_for(pr, op, g2).stats()["helper_launches"], lib=_lib.LIB_PATH)
 """
 
 
@@ -62,3 +66,8 @@ def test_handshake_bitwise_under_jitter():
     plain = _run({})
     np.testing.assert_array_equal(plain["sweep"], inline["sweep"])
     np.testing.assert_array_equal(jit["seq"], plain["seq"])
+    # the split tensor-core helpers of the sequential solver: deterministic under
+    # jitter, and the same sums as the inline far history up to rounding order
+    assert int(jit["helpers2"]) >= 1 and int(inline["helpers2"]) == 0
+    np.testing.assert_array_equal(jit["seq2"], plain["seq2"])
+    assert np.linalg.norm(plain["seq2"] - inline["seq2"]) <= 1e-12 * np.linalg.norm(inline["seq2"])

@@ -10,6 +10,7 @@ if [ "$1" = "build" ]; then
 fi
 rm -rf /tmp/ptime && mkdir -p /tmp/ptime && cp -r "$ROOT/paper_2510_11023_b200" "$ROOT/include" /tmp/ptime/
 cp "$ROOT/tools/variants/${PHASE_SO:-phase}.so" /tmp/ptime/paper_2510_11023_b200/libparafrac_b200.so
-sed "s#/root/repo#/tmp/ptime#" "$ROOT/tools/phases.py" > /tmp/ptime/phases.py
+SCRIPT=${PHASE_SCRIPT:-tools/phases.py}
+sed "s#/root/repo#/tmp/ptime#" "$ROOT/$SCRIPT" > /tmp/ptime/phases.py
 # one launch (no head start): slice 0 is block 0 of the sweep, the only CTA the timers follow
 PF_NO_HEADSTART=1 python /tmp/ptime/phases.py ${1:-3}
