@@ -245,6 +245,11 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   // helpers' part tiles [parity][batch][part][512], k_fine_sweep)
   const bool tc = c->kind == PF_SPACE_SINE1D && c->lgQ >= 10 && c->size % pf::TC_BATCH == 0;
   const size_t parts_len = (tc && hps > 1) ? (size_t)2 * (c->size / pf::TC_BATCH) * 8 * 512 : 0;
+  // far history of one-helper sweeps: measured at config 3 (profiles/r02_far_history_variants.txt)
+  // DFMA register tiles 8.8 ms, DMMA with direct loads 13.1 ms, DMMA + TMA bulk copies 10.1 ms
+  // per sweep: the DFMA tiles stay the default; PF_FAR_TC=1/2 select the others
+  int far_tc = 0;
+  if (const char* ft = std::getenv("PF_FAR_TC")) far_tc = (ft[0] == '1') ? 1 : (ft[0] == '2') ? 2 : 0;
   const size_t scr_stride = (size_t)2 * (hps + 1) * 2 * pf::HB * c->size + parts_len;
   if (c->scratch.ensure((size_t)bs * scr_stride)) return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
   const int nsync = bs * (2 + hps) + bs * 64;
@@ -259,6 +264,7 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   pf::Common cm = make_common(c);
   cm.m = m;
   cm.x_start = d_start;
+  cm.far_tc = far_tc;
   PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
   if (bs > 65535) return set_error(c, PF_ERR_UNSUPPORTED, "more than 65535 slices in one sweep launch");
   // Launch the sweep of slices [n_lo + s0, n_lo + s0 + ns) (local slices s0..) on stream st:

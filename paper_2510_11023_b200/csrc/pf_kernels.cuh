@@ -35,6 +35,10 @@ struct Common {
   // start state of the (single) slice when it differs from U[n]: fine_propagate's
   // `start` (stepping.py:170-171, path[0] = start; the bracket still uses U); nullptr = U[n]
   const double* x_start;
+  // far history of one-helper sweeps and of the inline path: 0 DFMA register
+  // tiles (default), 1 DMMA tensor cores, 2 DMMA fed by TMA bulk copies (helper);
+  // the sequential solver's split helpers always use DMMA (PF_FAR_TC, launch_fine)
+  int far_tc;
 };
 
 // Block length of the blocked L1 history: each history row is read once per
@@ -264,12 +268,12 @@ struct SweepSync {
 // k-step of 4 history rows and 8 modes, A[rr][k] = a_{R0+1+rr-(j0+k)} from
 // shared memory, B[k][n] = c_{j0+k}[8g+n] from global (L2 / HBM), the
 // accumulator C (8 target rows x 8 modes) in registers.
-// Canonical order, whoever computes it (slice CTA inline, its helper CTA, or
-// the split helpers of the sequential solver): the k-steps of a batch of 8
-// mode groups (64 modes) split into 8 interleaved parts (k-step s -> part
-// s mod 8), each accumulated in ascending s; out = b c_0 + (((P0 + P1) + ...) + P7).
-// (the sequential solver's split helpers sum sub-parts of a part first: same
-// terms, a different rounding order -- tested against the oracle, not bitwise)
+// Order: a batch of 8 mode groups (64 modes) accumulates every k-step in
+// ascending order in one warp, out = b c_0 + acc -- the same whether the slice
+// CTA computes it inline or its helper CTA does (bitwise, tested).  The
+// sequential solver's split helpers (far history of up to 64k rows over many
+// CTAs) sum interleaved parts instead: same terms, another rounding order
+// (tested against the inline path to 1e-12 and against the oracle).
 // ---------------------------------------------------------------------------
 constexpr int TC_BATCH = 64;          // modes per batch (8 groups of 8)
 constexpr int TC_RED = 8 * 8 * 64;    // doubles of the per-CTA part buffer (8 warps x 8 groups x 64)
@@ -280,9 +284,11 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-// One warp: the partial 8 x 64 tile of `batch` over k-steps s = s0, s0 + ds, ...
-// (rows j = 1 + 4 s + k <= J).  Lane l holds C rows l>>2, columns 2(l&3) + {0,1}
-// of each of the 8 groups.  Loads of the next k-step are in flight during the MMAs.
+// One warp: the 8 x 64 tile of `batch` accumulated over k-steps s = s0, s0 + ds, ...
+// (rows j = 1 + 4 s + k <= J), ascending.  Lane l holds C rows l>>2, columns
+// 2(l&3) + {0,1} of each of the 8 groups.  PD k-steps of loads are in flight
+// (register ring) while the MMAs of the current one issue.
+template <int PD = 8>
 __device__ __forceinline__ void tc_far_part(const double* __restrict__ path, int size, const double* __restrict__ aw,
                                             int R0, int J, int batch, int s0, int ds, double (&acc)[8][2]) {
   const int lane = threadIdx.x & 31, k = lane & 3, q = lane >> 2;
@@ -290,24 +296,148 @@ __device__ __forceinline__ void tc_far_part(const double* __restrict__ path, int
   for (int g = 0; g < 8; ++g) acc[g][0] = acc[g][1] = 0.0;
   const int nsteps = (J + 3) >> 2;
   const double* col = path + TC_BATCH * batch + q;
-  double an = 0.0, bn[8];
-  auto load = [&](int st, double& av, double (&bv)[8]) {
+  double av[PD], bv[PD][8];
+  auto load = [&](int st, double& a, double (&b)[8]) {
     const int j = 1 + 4 * st + k;
     const bool ok = j <= J;
-    av = ok ? aw[R0 + 1 + q - j] : 0.0;
+    a = ok ? aw[R0 + 1 + q - j] : 0.0;
     const double* row = col + (size_t)j * size;
 #pragma unroll
-    for (int g = 0; g < 8; ++g) bv[g] = ok ? __ldcg(row + 8 * g) : 0.0;
+    for (int g = 0; g < 8; ++g) b[g] = ok ? __ldcg(row + 8 * g) : 0.0;
   };
-  if (s0 < nsteps) load(s0, an, bn);
-  for (int st = s0; st < nsteps; st += ds) {
-    const double ac = an;
-    double bc[8];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) bc[g] = bn[g];
-    if (st + ds < nsteps) load(st + ds, an, bn);
+  for (int p = 0; p < PD; ++p) load(s0 + p * ds, av[p], bv[p]);
+  for (int st = s0; st < nsteps; st += PD * ds) {
 #pragma unroll
-    for (int g = 0; g < 8; ++g) dmma884(acc[g][0], acc[g][1], ac, bc[g]);
+    for (int p = 0; p < PD; ++p) {
+      if (st + p * ds < nsteps) {
+        const double ac = av[p];
+        double bc[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) bc[g] = bv[p][g];
+        load(st + (p + PD) * ds, av[p], bv[p]);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) dmma884(acc[g][0], acc[g][1], ac, bc[g]);
+      }
+    }
+  }
+}
+
+// a warp's finished tile of `batch` (every k-step in one accumulator) -> out rows
+__device__ __forceinline__ void tc_store_tile(const double (&acc)[8][2], const double* __restrict__ row0,
+                                              const double* __restrict__ bfine, int R0, int size, int batch,
+                                              double* out) {
+  const int lane = threadIdx.x & 31, rr = lane >> 2;
+  const double w = bfine[R0 + rr];
+#pragma unroll
+  for (int g = 0; g < 8; ++g)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int e = TC_BATCH * batch + 8 * g + 2 * (lane & 3) + i;
+      out[(size_t)rr * size + e] = w * __ldcg(row0 + e) + acc[g][i];
+    }
+}
+
+// ---- TMA staging (cp.async.bulk + mbarrier) of the history rows ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// bulk copy global -> shared (TMA), completion counted on `bar`
+__device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Helper CTA: the far-history tiles of block (R0, J) with the history rows
+// streamed through shared memory by TMA bulk copies: stages of 8 rows (one
+// 4 KB copy per row into a 64 B-padded slot: bank-conflict-free fragment
+// loads), NS stages in flight on mbarriers, thread 0 the producer.  Warp w
+// computes batch w over the k-steps in ascending order -- the arithmetic and
+// order of tc_far_block, so the tile is bitwise the inline one.
+struct TmaRing {
+  double* buf;                  // NS stages x 8 rows x (size + 8) doubles
+  unsigned long long* full;     // NS mbarriers
+  int NS;
+  long long issued;             // stages issued so far (running: mbarrier phases)
+};
+
+__device__ __forceinline__ void tc_far_block_tma(const double* __restrict__ path, const double* __restrict__ row0,
+                                                 int size, const double* __restrict__ aw,
+                                                 const double* __restrict__ bfine, int R0, int J, double* out,
+                                                 TmaRing& ring) {
+  const int NB = size / TC_BATCH, pitch = size + 8;
+  const int nstg = J / 8;  // J = (beta - 1) HB: whole stages of 8 rows
+  const long long g0 = ring.issued;
+  auto issue = [&](int i) {
+    const int slot = (int)((g0 + i) % ring.NS);
+    double* dst = ring.buf + (size_t)slot * 8 * pitch;
+    mbar_expect_tx(ring.full + slot, 8u * (unsigned)size * 8u);
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      tma_load(dst + (size_t)t * pitch, path + (size_t)(1 + 8 * i + t) * size, (unsigned)size * 8u, ring.full + slot);
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async;" ::: "memory");  // path rows (generic writes, acquired) -> bulk-copy reads
+    for (int i = 0; i < nstg && i < ring.NS; ++i) issue(i);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, k = lane & 3, q = lane >> 2;
+  double acc[8][2];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) acc[g][0] = acc[g][1] = 0.0;
+  for (int i = 0; i < nstg; ++i) {
+    const int slot = (int)((g0 + i) % ring.NS);
+    mbar_wait(ring.full + slot, (unsigned)(((g0 + i) / ring.NS) & 1));
+    const double* st = ring.buf + (size_t)slot * 8 * pitch;
+    if (w < NB) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int j = 1 + 8 * i + 4 * t + k;
+        const double a = aw[R0 + 1 + q - j];
+        const double* bp = st + (size_t)(4 * t + k) * pitch + TC_BATCH * w + q;
+        double bv[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) bv[g] = bp[8 * g];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) dmma884(acc[g][0], acc[g][1], a, bv[g]);
+      }
+    }
+    __syncthreads();  // every warp is done with the slot
+    if (threadIdx.x == 0 && i + ring.NS < nstg) issue(i + ring.NS);
+  }
+  ring.issued = g0 + nstg;
+  if (w < NB) tc_store_tile(acc, row0, bfine, R0, size, w, out);
+}
+
+// CTA (256 threads = 8 warps): the far-history tiles of every batch, warp w
+// computing batches w, w + 8, ... over all k-steps in ascending order (the
+// order of the slice CTA's inline path and of its helper CTA).
+__device__ __forceinline__ void tc_far_block(const double* __restrict__ path, const double* __restrict__ row0,
+                                             int size, const double* __restrict__ aw, const double* __restrict__ bfine,
+                                             int R0, int J, double* out) {
+  const int NB = size / TC_BATCH;
+  for (int batch = (int)(threadIdx.x >> 5); batch < NB; batch += 8) {
+    double acc[8][2];
+    tc_far_part(path, size, aw, R0, J, batch, 0, 1, acc);
+    tc_store_tile(acc, row0, bfine, R0, size, batch, out);
   }
 }
 
@@ -327,27 +457,7 @@ __device__ __forceinline__ void tc_out_index(int t, int i, int& slot, int& rr, i
   col = 8 * g + 2 * (lane & 3) + i;
 }
 
-// CTA (256 threads = 8 warps): the far-history tile of `batch` in canonical order,
-// warp w accumulating part w; written to out[rr * size + 64 batch + col].
-__device__ __forceinline__ void tc_far_batch(const double* __restrict__ path, const double* __restrict__ row0,
-                                             int size, const double* __restrict__ aw, const double* __restrict__ bfine,
-                                             int R0, int J, int batch, double* red, double* out) {
-  double acc[8][2];
-  tc_far_part(path, size, aw, R0, J, batch, (int)(threadIdx.x >> 5), 8, acc);
-  tc_store_part(red, acc);
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    int sl, rr, col;
-    tc_out_index((int)threadIdx.x, i, sl, rr, col);
-    const int e = TC_BATCH * batch + col;
-    double sum = red[sl];
-#pragma unroll
-    for (int w = 1; w < 8; ++w) sum += red[(size_t)w * 512 + sl];
-    out[(size_t)rr * size + e] = bfine[R0 + rr] * __ldcg(row0 + e) + sum;
-  }
-  __syncthreads();  // red is reused by the next batch
-}
+
 
 // Protocol stress build (-DPF_JITTER, tests/test_protocol_jitter.py): the
 // slice CTA delays its progress publish and the helper CTA its block by a
@@ -401,7 +511,8 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   // per slice: [parity][hps + 1][hist | bracket][HB][size]; tile hps is the combined one
   // (+ with split tensor-core helpers: the per-batch part tiles [parity][batch][part][512])
   const int NB = c.size / TC_BATCH;
-  const bool tc = NT == 256 && c.size % TC_BATCH == 0;  // far history on the FP64 tensor cores
+  // far history on the FP64 tensor cores: split helpers always, else when selected
+  const bool tc = NT == 256 && c.size % TC_BATCH == 0 && (hps > 1 || c.far_tc > 0);
   const size_t parts_len = (tc && hps > 1) ? (size_t)2 * NB * 8 * 512 : 0;
   double* scr = c.scratch + (size_t)b * ((size_t)2 * (hps + 1) * 2 * HB * c.size + parts_len);
   auto slot = [&](int parity, int h) { return scr + ((size_t)parity * (hps + 1) + h) * 2 * HB * c.size; };
@@ -412,17 +523,36 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     const double* aw = c.afine;
     const size_t aw_bytes = ((size_t)(c.m + HB + 1) * sizeof(double) + 15) & ~size_t(15);
     double* red = reinterpret_cast<double*>(smem);
+    size_t used = 0;
     if (aw_bytes + sizeof(double) * TC_RED <= (size_t)smem_total) {
       double* s_aw = reinterpret_cast<double*>(smem);
       for (int q = threadIdx.x; q <= c.m + HB; q += NT) s_aw[q] = c.afine[q];
       aw = s_aw;
       red = reinterpret_cast<double*>(smem + aw_bytes);
+      used = aw_bytes;
+    }
+    // the one helper of a slice streams the history rows by TMA (stages behind the weights)
+    TmaRing ring{nullptr, nullptr, 0, 0};
+    if (hps == 1 && c.far_tc == 2 && aw != c.afine) {
+      const size_t stage = sizeof(double) * 8 * (size_t)(c.size + 8);
+      const size_t avail = (size_t)smem_total - used - 128;
+      const int NS = (int)min((size_t)6, avail / stage);
+      if (NS >= 2) {
+        ring.full = reinterpret_cast<unsigned long long*>(smem + used);
+        ring.buf = reinterpret_cast<double*>(smem + used + 128);
+        ring.NS = NS;
+        if (threadIdx.x == 0) {
+          for (int i = 0; i < NS; ++i) mbar_init(ring.full + i, 1);
+          asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+      }
     }
     __syncthreads();
     __shared__ int s_abort;
     const int w = threadIdx.x >> 5;
     for (int beta = 0; beta < nblocks; ++beta) {
       const int J = far_extent(beta);
+      PF_TH(14);
       if (J > 0) {
         if (threadIdx.x == 0) {
           int ns = 32;  // the slice CTA publishes a huge progress when it aborts
@@ -436,12 +566,16 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         if (s_abort) return;
       }
       pf_jitter(b * 64 + hid, beta);
+      PF_TH(11);
       double* hs = slot(beta & 1, 0);
       const int R0 = beta * HB;
       const double* row0 = J > 0 ? path : (c.x_start ? c.x_start : U + (size_t)n * c.size);
-      if (hps == 1) {  // the slice's one helper: every batch, part p on warp p
-        for (int batch = 0; batch < NB; ++batch)
-          tc_far_batch(path, row0, c.size, aw, c.bfine, R0, J, batch, red, hs);
+      if (hps == 1) {  // the slice's one helper: batch w on warp w
+        if (ring.NS)
+          tc_far_block_tma(path, row0, c.size, aw, c.bfine, R0, J, hs, ring);
+        else
+          tc_far_block(path, row0, c.size, aw, c.bfine, R0, J, hs);
+        PF_TH(12);
         cta_publish_add(sync.ready + (size_t)b * hps, NB);
       } else {  // split helpers (sequential solver): unit (batch, part) -> helper unit mod hps
         for (int u = hid; u < NB * 8; u += hps) {
@@ -616,10 +750,9 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
           }
         }
         __syncthreads();
-      } else if (tc && red_off >= 0) {
-        double* red = reinterpret_cast<double*>(smem + red_off);
-        for (int batch = 0; batch < NB; ++batch)
-          tc_far_batch(path, path, c.size, c.afine, c.bfine, beta * HB, J, batch, red, s0);
+      } else if (tc) {
+        tc_far_block(path, path, c.size, c.afine, c.bfine, beta * HB, J, s0);
+        __syncthreads();  // the tile rows are read by other threads below
       } else if (helpers) {
         pf_jitter(b + 1000003, beta);
         cta_publish(sync.progress + b, r - 1);  // rows 0..r-1 are in the path

@@ -71,3 +71,20 @@ def test_handshake_bitwise_under_jitter():
     assert int(jit["helpers2"]) >= 1 and int(inline["helpers2"]) == 0
     np.testing.assert_array_equal(jit["seq2"], plain["seq2"])
     assert np.linalg.norm(plain["seq2"] - inline["seq2"]) <= 1e-12 * np.linalg.norm(inline["seq2"])
+
+
+@pytest.mark.parametrize("far_tc", ["1", "2"])
+def test_tensor_core_far_history_helper_bitwise_inline(far_tc):
+    """PF_FAR_TC=1 (DMMA, direct loads) / 2 (DMMA fed by TMA bulk copies): the
+    helper CTA's far history under jitter == the slice CTA's inline DMMA path,
+    bitwise, and the DFMA default to rounding."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a B200")
+    helper = _run({"PARAFRAC_B200_LIB": JITTER, "PF_FAR_TC": far_tc})
+    inline = _run({"PF_NO_HELPERS": "1", "PF_FAR_TC": "1"})
+    assert int(helper["helpers"]) >= 1 and int(inline["helpers"]) == 0
+    np.testing.assert_array_equal(helper["sweep"], inline["sweep"])
+    dfma = _run({})
+    assert np.linalg.norm(helper["sweep"] - dfma["sweep"]) <= 1e-13 * np.linalg.norm(dfma["sweep"])
