@@ -14,9 +14,9 @@ asserts block-split invariance bitwise (``test_stepping.py:166-175``), and
 ``oracle.block_bounds`` is its rule, so the iterate is the serial one.
 
 Fixture (``tests/golden/oracle_cfg<i>_2d[_nt<P>].npz``), sized for git:
-  nodes            node indices stored in full (every ``stride``-th and the last)
+  nodes            node indices stored in full (every ``stride``-th, default P/8, and the last)
   states, fine     the final iterate and F_old at those nodes
-  states_k1/k2     the iterate after iterations 1 and 2 at those nodes
+  states_k2        the iterate after iteration 2 at those nodes
   proj             every node of the final iterate projected on 8 seeded
                    Gaussian vectors (catches a mismatch at any node)
   norms            Euclidean norm of every node of the final iterate
@@ -115,7 +115,7 @@ def main():
             diffs.append(diff)
             u_curr = u_next
             iterations = k + 1
-            if k < 2:
+            if k == 1:
                 snaps[k + 1] = u_curr.copy()
             print(f"iteration {k + 1}: diff {diff:.3e} ({time.time() - t0:.0f} s, "
                   f"pcg mean {np.mean(pcg):.2f})", flush=True)
