@@ -99,6 +99,15 @@ struct pf_ctx {
   int num_sms = 0;
   int allow_helpers = 1;  // PF_NO_HELPERS=1 forces the inline far history
   int last_helpers = 0;
+  // pipelined parareal driver (1-D): second F_old buffer, per-parity sweep status,
+  // correction chunk state, cancel word, chunk streams and events
+  DevBuf fold2;
+  Status* d_status2 = nullptr;
+  Status* d_corr_status = nullptr;
+  int* d_corr_state = nullptr;  // [parity][4]: same, first changed, failed
+  int* d_cancel = nullptr;
+  cudaStream_t pstream[8] = {};
+  cudaEvent_t ev_sw[2][8] = {}, ev_co[2][8] = {}, ev_init = nullptr;
   Engine2D* e2 = nullptr;   // PF_SPACE_SINE2D only
   Engine2D* e2c = nullptr;  // batch-1 engine of the graph-captured sequential sweeps (stable buffers)
 };
@@ -230,8 +239,19 @@ int ensure_status(pf_ctx* c, int n) {
 #ifndef PF_BRK_EM
 #define PF_BRK_EM 2  // modes per thread of k_bracket_all
 #endif
+// Options of the pipelined parareal driver's sweep launches: buffers at slot
+// offsets of a fixed capacity (chunks of one sweep run concurrently on their own
+// streams), the frozen-prefix skip and the cancel word (k_fine_sweep).
+struct FineOpts {
+  int slot0 = 0, cap = 0;
+  cudaStream_t stream = nullptr;
+  const int* frozen_from = nullptr;
+  const double* fold_prev = nullptr;
+  const int* cancel = nullptr;
+};
+
 int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, Status* d_st, int m_override = 0,
-                int hps_req = 1, const double* d_start = nullptr) {
+                int hps_req = 1, const double* d_start = nullptr, const FineOpts* fo = nullptr) {
   if (d_start && bs != 1) return set_error(c, PF_ERR_ARGUMENT, "a start state needs a single-slice sweep");
   if (c->kind == PF_SPACE_SINE2D) {
     // the parareal driver's own sweeps (states == U) warm-start from the previous sweep
@@ -240,7 +260,15 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   }
   const int m = m_override > 0 ? m_override : c->grid.m;
   const int hps = std::max(1, hps_req);
-  if (c->paths.ensure((size_t)bs * (m + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "paths");
+  const int slot0 = fo ? fo->slot0 : 0, cap = fo ? std::max(fo->cap, fo->slot0 + bs) : bs;
+  cudaStream_t stream_keep = c->stream;
+  if (fo && fo->stream) c->stream = fo->stream;
+  struct Restore {
+    pf_ctx* c;
+    cudaStream_t s;
+    ~Restore() { c->stream = s; }
+  } restore{c, stream_keep};
+  if (c->paths.ensure((size_t)cap * (m + 1) * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "paths");
   // per slice: block tiles [parity][hps + 1][2][HB][size] (+ the split tensor-core
   // helpers' part tiles [parity][batch][part][512], k_fine_sweep)
   const bool tc = c->kind == PF_SPACE_SINE1D && c->lgQ >= 10 && c->size % pf::TC_BATCH == 0;
@@ -251,31 +279,46 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   int far_tc = 0;
   if (const char* ft = std::getenv("PF_FAR_TC")) far_tc = (ft[0] == '1') ? 1 : (ft[0] == '2') ? 2 : 0;
   const size_t scr_stride = (size_t)2 * (hps + 1) * 2 * pf::HB * c->size + parts_len;
-  if (c->scratch.ensure((size_t)bs * scr_stride)) return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
-  const int nsync = bs * (2 + hps) + bs * 64;
+  if (c->scratch.ensure((size_t)cap * scr_stride)) return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
+  // sync words: progress[cap] | ready[cap * hps] | abort[cap] | tickets[cap * 64]
+  const int nsync = cap * (2 + hps) + cap * 64;
   if (c->sync_cap < nsync) {
+    if (fo) PF_CUDA(c, cudaDeviceSynchronize());  // concurrent chunk launches may still use the old words
     if (c->d_sync) cudaFree(c->d_sync);
     c->d_sync = nullptr;
     c->sync_cap = 0;
     PF_CUDA(c, cudaMalloc(&c->d_sync, sizeof(int) * nsync));
     c->sync_cap = nsync;
   }
-  PF_CUDA(c, cudaMemsetAsync(c->d_sync, 0, sizeof(int) * nsync, c->stream));
+  int* sy_progress = c->d_sync;
+  int* sy_ready = c->d_sync + cap;
+  int* sy_abort = c->d_sync + cap + (size_t)cap * hps;
+  int* sy_tickets = c->d_sync + 2 * cap + (size_t)cap * hps;
+  PF_CUDA(c, cudaMemsetAsync(sy_progress + slot0, 0, sizeof(int) * bs, c->stream));
+  PF_CUDA(c, cudaMemsetAsync(sy_ready + (size_t)slot0 * hps, 0, sizeof(int) * bs * hps, c->stream));
+  PF_CUDA(c, cudaMemsetAsync(sy_abort + slot0, 0, sizeof(int) * bs, c->stream));
+  PF_CUDA(c, cudaMemsetAsync(sy_tickets + (size_t)slot0 * 64, 0, sizeof(int) * bs * 64, c->stream));
   pf::Common cm = make_common(c);
   cm.m = m;
   cm.x_start = d_start;
   cm.far_tc = far_tc;
-  PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+  if (fo) {
+    cm.frozen_from = fo->frozen_from;
+    cm.fold_prev = fo->fold_prev;
+    cm.cancel = fo->cancel;
+  }
+  if (!fo) PF_CUDA(c, cudaEventRecord(c->ev0, c->stream));
   if (bs > 65535) return set_error(c, PF_ERR_UNSUPPORTED, "more than 65535 slices in one sweep launch");
   // Launch the sweep of slices [n_lo + s0, n_lo + s0 + ns) (local slices s0..) on stream st:
   // per-slice sync flags, paths, scratch, outputs and status at the local offsets.
   auto sweep = [&](int s0, int ns, cudaStream_t st, const double* brk) -> int {
     pf::Common cl = cm;
-    cl.scratch = c->scratch.p + (size_t)s0 * scr_stride;
+    const size_t q0 = (size_t)slot0 + s0;  // buffer slot of local slice s0
+    cl.scratch = c->scratch.p + q0 * scr_stride;
     cl.brk = brk;
-    pf::SweepSync sync{c->d_sync + s0, c->d_sync + bs + (size_t)s0 * hps, c->d_sync + bs + (size_t)bs * hps + s0,
-                       c->d_sync + 2 * bs + (size_t)bs * hps + (size_t)s0 * 64};
-    double* dp = c->paths.p + (size_t)s0 * (m + 1) * c->size;
+    if (cl.fold_prev) cl.fold_prev += (size_t)s0 * c->size;
+    pf::SweepSync sync{sy_progress + q0, sy_ready + q0 * hps, sy_abort + q0, sy_tickets + q0 * 64};
+    double* dp = c->paths.p + q0 * (m + 1) * c->size;
     double* dout = d_out ? d_out + (size_t)s0 * c->size : nullptr;
     Status* dst = d_st + s0;
     int nl = n_lo + s0;
@@ -316,13 +359,14 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
     return 0;
   };
   // bracket rows of slices [n_lo + s0, n_lo + bs): one batched GEMM (k_bracket_all)
+  if (c->brk.ensure((size_t)cap * m * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "bracket");
+  double* brk0 = c->brk.p + (size_t)slot0 * m * c->size;
   auto bracket = [&](int s0, cudaStream_t st) -> int {
     const int ns = bs - s0;
     if (n_lo + s0 + ns <= 1) return 0;  // only slice 0: no coarse history
-    if (c->brk.ensure((size_t)ns * m * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "bracket");
     constexpr int RT = PF_BRK_RT, EM = PF_BRK_EM;
     const dim3 gb((unsigned)((c->size + 256 * EM - 1) / (256 * EM)), (unsigned)((m + RT - 1) / RT), (unsigned)ns);
-    pf::k_bracket_all<RT, EM><<<gb, 256, 0, st>>>(cm, d_u, n_lo + s0, c->brk.p);
+    pf::k_bracket_all<RT, EM><<<gb, 256, 0, st>>>(cm, d_u, n_lo + s0, brk0);
     c->stats.kernel_launches += 1;
     return 0;
   };
@@ -333,7 +377,8 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   // Only where the bracket kernel is long enough to pay for the second launch
   // (config 3: 2^25 bracket entries; config 2's 2^18 measured slower).
   const bool big = (double)m * c->size * bs >= 16777216.0;
-  const bool head = big && n_lo == 0 && bs >= 2 && m_override == 0 && c->allow_helpers && !(nohs && nohs[0] == '1');
+  const bool head = !fo && big && n_lo == 0 && bs >= 2 && m_override == 0 && c->allow_helpers &&
+                    !(nohs && nohs[0] == '1');
   if (head) {
     if (!c->side_stream) {
       PF_CUDA(c, cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
@@ -345,16 +390,18 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
     if (sweep(0, 1, c->side_stream, nullptr)) return c->err.code;
     PF_CUDA(c, cudaEventRecord(c->ev_join, c->side_stream));
     if (bracket(1, c->stream)) return c->err.code;
-    if (sweep(1, bs - 1, c->stream, c->brk.p)) return c->err.code;
+    if (sweep(1, bs - 1, c->stream, brk0)) return c->err.code;
     PF_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
   } else {
     if (bracket(0, c->stream)) return c->err.code;
-    if (sweep(0, bs, c->stream, (n_lo + bs > 1) ? c->brk.p : nullptr)) return c->err.code;
+    if (sweep(0, bs, c->stream, (n_lo + bs > 1) ? brk0 : nullptr)) return c->err.code;
   }
   PF_CUDA(c, cudaGetLastError());
-  PF_CUDA(c, cudaEventRecord(c->ev1, c->stream));
-  c->stats.fine_launches += 1;
-  c->stats.helper_launches += c->last_helpers ? 1 : 0;  // one sweep, however many launches
+  if (!fo) {  // (the pipelined driver counts its chunked sweeps itself)
+    PF_CUDA(c, cudaEventRecord(c->ev1, c->stream));
+    c->stats.fine_launches += 1;
+    c->stats.helper_launches += c->last_helpers ? 1 : 0;  // one sweep, however many launches
+  }
   return 0;
 }
 
@@ -721,6 +768,17 @@ void pf_destroy(pf_ctx* c) {
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  c->fold2.release();
+  for (void* p : {(void*)c->d_status2, (void*)c->d_corr_status, (void*)c->d_corr_state, (void*)c->d_cancel})
+    if (p) cudaFree(p);
+  for (cudaStream_t s : c->pstream)
+    if (s) cudaStreamDestroy(s);
+  for (int q = 0; q < 2; ++q)
+    for (int i = 0; i < 8; ++i) {
+      if (c->ev_sw[q][i]) cudaEventDestroy(c->ev_sw[q][i]);
+      if (c->ev_co[q][i]) cudaEventDestroy(c->ev_co[q][i]);
+    }
+  if (c->ev_init) cudaEventDestroy(c->ev_init);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c->e2;
@@ -961,6 +1019,7 @@ int pf_dev_parareal_init(pf_ctx* c, const double* u0) {
   for (DevBuf* b : {&c->U, &c->Unext}) if (b->ensure(rows * sz)) return cuda_fail(c, cudaErrorMemoryAllocation, "U");
   for (DevBuf* b : {&c->fold, &c->gold, &c->gnew}) if (b->ensure((rows - 1) * sz)) return cuda_fail(c, cudaErrorMemoryAllocation, "G");
   if (c->scalar.ensure(8)) return cuda_fail(c, cudaErrorMemoryAllocation, "scalar");
+  if (!c->d_corr_state) PF_CUDA(c, cudaMalloc(&c->d_corr_state, 8 * sizeof(int)));
   if (upload(c, c->U.p, u0, sz)) return c->err.code;
   int rc = run_coarse_dev(c, c->U.p);
   if (rc) return rc;
@@ -991,6 +1050,7 @@ int pf_dev_parareal_correct(pf_ctx* c, const double* d_fold, int k, double* diff
   a.gnew = c->gnew.p;
   a.unext = c->Unext.p;
   a.out = c->scalar.p;
+  a.state = c->d_corr_state;
   // From the second iteration on, G_old is the previous sweep's G_new, which
   // is bitwise what parareal.py:78-79 recomputes.
   if (k > 0) std::swap(c->gold, c->gnew);
@@ -1034,6 +1094,207 @@ int pf_dev_parareal_read(pf_ctx* c, double* states, double* coarse_new, double* 
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined parareal (parareal.py:111-137): the slices are cut
+// into C contiguous chunks; the correction sweep of iteration k runs chunk by
+// chunk (k_coarse CM_CORRECT over a node range, its frozen-prefix state carried
+// between chunk launches), and chunk c of the fine sweep of iteration k+1
+// starts on its own stream as soon as the correction has finalised its nodes
+// (U^{k+1}_0..n of every slice n in the chunk), i.e. while the correction of
+// the later chunks still runs.  That sweep is launched before the host knows
+// whether iteration k met the tolerance: if it did, the host sets the cancel
+// word and the speculative sweep stops at its next block boundary; its F_old
+// goes to the other of two buffers, so iteration k's results stand.  Slices of
+// the frozen prefix copy their F_old row (k_fine_sweep) or, for whole chunks
+// below the previous prefix, are copied by the host.  Same kernels on the same
+// inputs as the sequential driver: bitwise the same iterates, diffs and
+// iteration count (tests/test_gpu_parity.py).  PF_PIPELINE=C sets the chunk
+// count (0 or 1: the sequential driver).
+// ---------------------------------------------------------------------------
+int pipeline_chunks(const pf_ctx* c) {
+  if (c->kind != PF_SPACE_SINE1D) return 0;
+  int C = 4;
+  if (const char* env = std::getenv("PF_PIPELINE")) C = std::atoi(env);
+  C = std::min(std::min(C, 8), c->grid.nt / 2);
+  return C >= 2 ? C : 0;
+}
+
+int parareal_pipelined(pf_ctx* c, int C, double tol, int k_max, const double* reference, double* diffs,
+                       double* iteration_times, double* errors, int* iterations, int* stop_reason,
+                       std::chrono::steady_clock::time_point t0, double*& fold_final) {
+  const int nt = c->grid.nt;
+  const size_t sz = c->size;
+  if (c->fold2.ensure((size_t)nt * sz)) return cuda_fail(c, cudaErrorMemoryAllocation, "fold2");
+  if (!c->d_status2) PF_CUDA(c, cudaMalloc(&c->d_status2, sizeof(Status) * c->status_cap));
+  if (!c->d_corr_status) PF_CUDA(c, cudaMalloc(&c->d_corr_status, sizeof(Status)));
+  if (!c->d_cancel) PF_CUDA(c, cudaMalloc(&c->d_cancel, sizeof(int)));
+  if (!c->ev_init) {
+    PF_CUDA(c, cudaEventCreateWithFlags(&c->ev_init, cudaEventDisableTiming));
+    for (int i = 0; i < 8; ++i) {
+      PF_CUDA(c, cudaStreamCreateWithFlags(&c->pstream[i], cudaStreamNonBlocking));
+      for (int q = 0; q < 2; ++q) {
+        PF_CUDA(c, cudaEventCreateWithFlags(&c->ev_sw[q][i], cudaEventDisableTiming));
+        PF_CUDA(c, cudaEventCreateWithFlags(&c->ev_co[q][i], cudaEventDisableTiming));
+      }
+    }
+  }
+  std::vector<int> cb(C + 1);  // contiguous near-even chunks (parareal._block_bounds)
+  for (int i = 0, lo = 0; i < C; ++i) {
+    cb[i] = lo;
+    lo += nt / C + (i < nt % C ? 1 : 0);
+  }
+  cb[C] = nt;
+  double* F[2] = {c->fold.p, c->fold2.p};
+  Status* SS[2] = {c->d_status, c->d_status2};
+  PF_CUDA(c, cudaMemsetAsync(c->d_cancel, 0, sizeof(int), c->stream));
+  PF_CUDA(c, cudaEventRecord(c->ev_init, c->stream));
+  // sweep of iteration k (parity q) for chunk ch on stream ps[ch], reading states U
+  auto sweep_chunk = [&](int k, int ch, const double* U, int frozen_prev) -> int {
+    const int q = k & 1, lo = cb[ch], bs = cb[ch + 1] - cb[ch];
+    cudaStream_t ps = c->pstream[ch];
+    if (k > 0 && cb[ch + 1] <= frozen_prev) {  // the whole chunk is frozen: its F_old rows stand
+      PF_CUDA(c, cudaMemcpyAsync(F[q] + (size_t)lo * sz, F[q ^ 1] + (size_t)lo * sz, (size_t)bs * sz * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, ps));
+      PF_CUDA(c, cudaMemsetAsync(SS[q] + lo, 0, sizeof(Status) * bs, ps));
+    } else {
+      FineOpts fo;
+      fo.slot0 = lo;
+      fo.cap = nt;
+      fo.stream = ps;
+      fo.cancel = c->d_cancel;
+      if (k > 0) {
+        fo.frozen_from = c->d_corr_state + 4 * (q ^ 1) + 1;  // the first node correction k-1 changed
+        fo.fold_prev = F[q ^ 1] + (size_t)lo * sz;
+      }
+      int rc = launch_fine(c, U, lo, bs, F[q] + (size_t)lo * sz, SS[q] + lo, 0, 1, nullptr, &fo);
+      if (rc) return rc;
+    }
+    PF_CUDA(c, cudaEventRecord(c->ev_sw[q][ch], ps));
+    return 0;
+  };
+  auto cancel_all = [&]() {
+    const int one = 1;
+    cudaMemcpyAsync(c->d_cancel, &one, sizeof(int), cudaMemcpyHostToDevice, c->stream);
+    cudaStreamSynchronize(c->stream);
+    for (int i = 0; i < C; ++i) cudaStreamSynchronize(c->pstream[i]);
+  };
+  for (int ch = 0; ch < C; ++ch) {
+    PF_CUDA(c, cudaStreamWaitEvent(c->pstream[ch], c->ev_init, 0));
+    if (int rc = sweep_chunk(0, ch, c->U.p, 0)) return rc;
+  }
+  std::vector<double> last(sz), tmp(sz);
+  std::vector<Status> hst(nt);
+  int iters = 0, stop = 0, frozen_prev = 0;
+  for (int k = 0; k < k_max; ++k) {
+    const int q = k & 1;
+    // correction k, chunk by chunk, each after the sweep chunk it consumes
+    if (k > 0) std::swap(c->gold, c->gnew);
+    for (int ch = 0; ch < C; ++ch) {
+      PF_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_sw[q][ch], 0));
+      pf::CoarseArgs a{};
+      a.mode = pf::CM_CORRECT;
+      a.k_iter = k;
+      a.guard = c->guard;
+      a.ucur = c->U.p;
+      a.fold = F[q];
+      a.gold = c->gold.p;
+      a.gnew = c->gnew.p;
+      a.unext = c->Unext.p;
+      a.out = c->scalar.p;
+      a.n_begin = cb[ch];
+      a.n_end = cb[ch + 1];
+      a.state = c->d_corr_state + 4 * q;
+      if (int rc = launch_coarse(c, a, c->d_corr_status)) return rc;
+      PF_CUDA(c, cudaEventRecord(c->ev_co[q][ch], c->stream));
+    }
+    // speculative sweep k+1 on U^{k+1}, chunk ch as soon as correction chunk ch is done
+    if (k + 1 < k_max)
+      for (int ch = 0; ch < C; ++ch) {
+        PF_CUDA(c, cudaStreamWaitEvent(c->pstream[ch], c->ev_co[q][ch], 0));
+        if (int rc = sweep_chunk(k + 1, ch, c->Unext.p, frozen_prev)) return rc;
+      }
+    double h[2] = {0.0, 0.0};
+    Status cs{};
+    PF_CUDA(c, cudaMemcpyAsync(h, c->scalar.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    PF_CUDA(c, cudaMemcpyAsync(&cs, c->d_corr_status, sizeof(Status), cudaMemcpyDeviceToHost, c->stream));
+    PF_CUDA(c, cudaMemcpyAsync(hst.data(), SS[q], sizeof(Status) * nt, cudaMemcpyDeviceToHost, c->stream));
+    PF_CUDA(c, cudaStreamSynchronize(c->stream));  // correction k, hence every chunk of sweep k, is done
+    // the sweep's failure first (parareal.py:75-88 raises before the correction)
+    for (int n = 0; n < nt; ++n) {
+      c->stats.pcg_iterations += hst[n].iters;
+      c->stats.solves += hst[n].solves;
+    }
+    for (int n = 0; n < nt; ++n) {
+      const Status& s1 = hst[n];
+      if (s1.code == pf::ST_OK) continue;
+      int best = n;
+      for (int j = n + 1; j < nt; ++j)
+        if (hst[j].code != pf::ST_OK &&
+            (hst[j].r < hst[best].r ||
+             (hst[j].r == hst[best].r && hst[j].code == pf::ST_COEFF && hst[best].code != pf::ST_COEFF)))
+          best = j;
+      cancel_all();
+      c->err = pf_error{};
+      c->err.step_n = 0;  // the reference's block [0, nt) (threads = 1)
+      c->err.step_r = hst[best].r;
+      if (hst[best].code == pf::ST_COEFF) {
+        c->err.code = PF_ERR_COEFFICIENT;
+        c->err.node = hst[best].node;
+        std::snprintf(c->err.message, sizeof(c->err.message), "diffusion coefficient is not finite");
+      } else {
+        c->err.code = PF_ERR_SOLVER;
+        std::snprintf(c->err.message, sizeof(c->err.message), "fine-sweep solve failed (interval %d)", hst[best].n);
+      }
+      return c->err.code;
+    }
+    c->stats.pcg_iterations += cs.iters;
+    c->stats.solves += cs.solves;
+    c->stats.fine_launches += 1;
+    if (cs.code != pf::ST_OK) {
+      cancel_all();
+      c->err = pf_error{};
+      c->err.step_r = -1;
+      if (cs.code == pf::ST_DIVERGE) {
+        c->err.code = PF_ERR_DIVERGENCE;
+        c->err.iteration = k;
+        c->err.interval = cs.n;
+        std::snprintf(c->err.message, sizeof(c->err.message), "%s",
+                      cs.r == 0 ? "non-finite state after correction sweep" : "state norm exceeds divergence guard");
+      } else {
+        c->err.code = cs.code == pf::ST_COEFF ? PF_ERR_COEFFICIENT : PF_ERR_SOLVER;
+        c->err.node = cs.node;
+        c->err.step_n = cs.n;
+        std::snprintf(c->err.message, sizeof(c->err.message), "singular or ill-conditioned time-step system");
+      }
+      return c->err.code;
+    }
+    const double diff = h[0];
+    c->warm_diff = diff;
+    c->frozen = std::min((int)h[1], nt);
+    frozen_prev = c->frozen;
+    std::swap(c->U, c->Unext);  // u_curr = u_next (parareal.py:133)
+    if (diffs) diffs[k] = diff;
+    if (iteration_times)
+      iteration_times[k] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (reference && errors) {
+      if (download(c, last.data(), c->U.p + (size_t)nt * sz, sz)) return c->err.code;
+      PF_CUDA(c, cudaStreamSynchronize(c->stream));
+      for (size_t i = 0; i < sz; ++i) tmp[i] = last[i] - reference[(size_t)nt * sz + i];
+      errors[k + 1] = host_norm(c, tmp.data());
+    }
+    iters = k + 1;
+    fold_final = F[q];
+    if (tol > 0 && diff < tol) {
+      stop = 1;
+      break;
+    }
+  }
+  cancel_all();  // the speculative sweep after the last iteration
+  if (iterations) *iterations = iters;
+  if (stop_reason) *stop_reason = stop;
+  return 0;
+}
+
 int pf_parareal(pf_ctx* c, const double* u0, double tol, int k_max, const double* reference, double* states,
                 double* coarse_new, double* coarse_old, double* fine_endpoints, double* diffs,
                 double* iteration_times, double* errors, int* iterations, int* stop_reason) {
@@ -1052,6 +1313,18 @@ int pf_parareal(pf_ctx* c, const double* u0, double tol, int k_max, const double
     errors[0] = host_norm(c, tmp.data());
   }
   int iters = 0, stop = 0;
+  if (const int C = pipeline_chunks(c)) {
+    double* fold_final = c->fold.p;
+    rc = parareal_pipelined(c, C, tol, k_max, reference, diffs, iteration_times, errors, &iters, &stop, t0,
+                            fold_final);
+    if (rc) return rc;
+    if (fine_endpoints && download(c, fine_endpoints, fold_final, (size_t)nt * sz)) return c->err.code;
+    rc = pf_dev_parareal_read(c, states, coarse_new, coarse_old);
+    if (rc) return rc;
+    if (iterations) *iterations = iters;
+    if (stop_reason) *stop_reason = stop;
+    return 0;
+  }
   for (int k = 0; k < k_max; ++k) {
     // slices below the frozen prefix have bitwise the inputs of their last
     // sweep: their F_old rows stand (see k_coarse CM_CORRECT)

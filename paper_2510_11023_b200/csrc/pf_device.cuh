@@ -66,7 +66,7 @@ __device__ __forceinline__ void dft4(cd& a0, cd& a1, cd& a2, cd& a3) {
 // ---------------------------------------------------------------------------
 // status: one word per CTA, decoded on the host into pf_error
 // ---------------------------------------------------------------------------
-enum StatusCode : int { ST_OK = 0, ST_SOLVER = 2, ST_COEFF = 3, ST_DIVERGE = 4 };
+enum StatusCode : int { ST_OK = 0, ST_SOLVER = 2, ST_COEFF = 3, ST_DIVERGE = 4, ST_CANCEL = 9 };
 
 struct Status {
   int code;   // StatusCode

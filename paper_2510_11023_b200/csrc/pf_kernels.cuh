@@ -39,6 +39,14 @@ struct Common {
   // tiles (default), 1 DMMA tensor cores, 2 DMMA fed by TMA bulk copies (helper);
   // the sequential solver's split helpers always use DMMA (PF_FAR_TC, launch_fine)
   int far_tc;
+  // pipelined parareal (pf_parareal): a slice below *frozen_from
+  // (the first node the previous correction changed) has bitwise the inputs of
+  // its last sweep -- it copies its F_old row from fold_prev instead of sweeping;
+  // *cancel (set by the host when the iteration before converged) ends a
+  // speculative sweep at its next block boundary.  nullptr: off.
+  const int* frozen_from;
+  const double* fold_prev;
+  const int* cancel;
 };
 
 // Block length of the blocked L1 history: each history row is read once per
@@ -685,6 +693,24 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     t_entry = (long long)t0;
   }
+  if (c.frozen_from && n < *c.frozen_from) {
+    // frozen prefix (pipelined driver): the last correction left U_0..U_n bitwise
+    // unchanged, so this slice's F_old row stands -- copied, not recomputed
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = threadIdx.x + i * NT;
+      if (e < c.size) out[(size_t)b * c.size + e] = c.fold_prev[(size_t)b * c.size + e];
+    }
+    if (threadIdx.x == 0) {
+      if (helpers) {
+        st_release(sync.abort + b, 1);  // the helper sees it and exits
+        st_release(sync.progress + b, 0x3fffffff);
+      }
+      Status fz = {ST_OK, n, 0, -1, 0, 0, {0, 0}, t_entry, t_entry};
+      status[b] = fz;
+    }
+    return;
+  }
   SP sp;
   sp.init(smem, spp);
   double* ring = ring_off >= 0 ? reinterpret_cast<double*>(smem + ring_off) : nullptr;
@@ -736,6 +762,12 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     const int rr = (r - 1) % HB;
     const int beta = (r - 1) / HB;
     PF_T(10);
+    if (c.cancel && rr == 0 && beta > 0 &&
+        __syncthreads_or(threadIdx.x == 0 && *(volatile const int*)c.cancel != 0)) {
+      st.code = ST_CANCEL;  // speculative sweep after convergence: discarded
+      st.r = r;
+      break;
+    }
     if (rr == 0) {
       J = far_extent(beta);
       double* s0 = slot(beta & 1, 0);
@@ -932,6 +964,11 @@ struct CoarseArgs {
   double* gnew;
   double* unext;
   double* out;       // CM_SINGLE result; CM_CORRECT: out[0] = diff
+  // CM_CORRECT over nodes [n_begin, n_end) (n_end = 0: all); the frozen-prefix
+  // state crosses chunk launches in state[0] (same), [1] (first changed node),
+  // [2] (a chunk failed: later chunks do nothing); guards + diff in the last chunk
+  int n_begin, n_end;
+  int* state;
 };
 
 template <class SP, class SPP, int NT, int EPT>
@@ -968,10 +1005,14 @@ __global__ void __launch_bounds__(NT) k_coarse(Common c, SPP spp, CoarseArgs a, 
       }
     }
   } else {  // CM_CORRECT (parareal.py:114-128)
+    const int nb = a.n_begin, ne = a.n_end > 0 ? a.n_end : c.nt;
+    if (nb > 0 && a.state[2] != 0) return;  // an earlier chunk failed and reported
+    if (nb == 0) {
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-      const int e = threadIdx.x + i * NT;
-      if (e < c.size) a.unext[e] = a.ucur[e];
+      for (int i = 0; i < EPT; ++i) {
+        const int e = threadIdx.x + i * NT;
+        if (e < c.size) a.unext[e] = a.ucur[e];
+      }
     }
     // Frozen prefix: while U_next[0..n] equals U_cur[0..n] bitwise, the coarse
     // step of node n has exactly G_old[n]'s inputs (G_old is the previous
@@ -979,9 +1020,9 @@ __global__ void __launch_bounds__(NT) k_coarse(Common c, SPP spp, CoarseArgs a, 
     // finite-termination structure of parareal.py:114-118, exploited exactly.
     // `same` is CTA-uniform (__syncthreads_and); first_changed = the first node
     // whose state this sweep changed (the next fine sweep starts there).
-    bool same = true;
-    int first_changed = c.nt + 1;
-    for (int n = 0; n < c.nt; ++n) {
+    bool same = nb == 0 || a.state[0] != 0;
+    int first_changed = nb == 0 ? c.nt + 1 : a.state[1];
+    for (int n = nb; n < ne; ++n) {
       st.n = n;
       if (same && n > 0) {
         int eq = 1;
@@ -1018,6 +1059,15 @@ __global__ void __launch_bounds__(NT) k_coarse(Common c, SPP spp, CoarseArgs a, 
           a.unext[o + c.size] = a.fold[o] + (x[i] - a.gold[o]);
         }
       }
+    }
+    if (ne < c.nt) {  // chunk boundary: hand the state to the next chunk launch
+      if (threadIdx.x == 0) {
+        a.state[0] = same ? 1 : 0;
+        a.state[1] = first_changed;
+        a.state[2] = st.code != ST_OK;
+        if (st.code != ST_OK) status[0] = st;
+      }
+      return;
     }
     if (same && st.code == ST_OK) {  // last node
       int eq = 1;
@@ -1071,6 +1121,7 @@ __global__ void __launch_bounds__(NT) k_coarse(Common c, SPP spp, CoarseArgs a, 
       if (threadIdx.x == 0) {
         a.out[0] = dmax;
         a.out[1] = (double)first_changed;
+        a.state[1] = first_changed;
       }
     }
   }
