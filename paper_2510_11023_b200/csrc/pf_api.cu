@@ -1220,10 +1220,13 @@ int parareal_pipelined(pf_ctx* c, int C, double tol, int k_max, const double* re
     PF_CUDA(c, cudaMemcpyAsync(hst.data(), SS[q], sizeof(Status) * nt, cudaMemcpyDeviceToHost, c->stream));
     PF_CUDA(c, cudaStreamSynchronize(c->stream));  // correction k, hence every chunk of sweep k, is done
     // the sweep's failure first (parareal.py:75-88 raises before the correction)
+    bool swept = false;  // some slice of sweep k was not frozen (the sequential driver's launch count)
     for (int n = 0; n < nt; ++n) {
       c->stats.pcg_iterations += hst[n].iters;
       c->stats.solves += hst[n].solves;
+      swept |= hst[n].solves > 0;
     }
+    if (swept) c->stats.fine_launches += 1;
     for (int n = 0; n < nt; ++n) {
       const Status& s1 = hst[n];
       if (s1.code == pf::ST_OK) continue;
@@ -1249,7 +1252,6 @@ int parareal_pipelined(pf_ctx* c, int C, double tol, int k_max, const double* re
     }
     c->stats.pcg_iterations += cs.iters;
     c->stats.solves += cs.solves;
-    c->stats.fine_launches += 1;
     if (cs.code != pf::ST_OK) {
       cancel_all();
       c->err = pf_error{};
