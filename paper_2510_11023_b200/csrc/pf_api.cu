@@ -328,17 +328,14 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
       // shared-memory ring of the last NR states behind the space's own smem
       const size_t ring_bytes = sizeof(double) * pf::NR * c->size;
       const size_t base = (c->smem + 15) & ~size_t(15);
-      int ring_off = -1, red_off = -1;
+      int ring_off = -1;
       size_t smem = c->smem;
       if (base + ring_bytes <= 227 * 1024) {
         ring_off = (int)base;
         smem = base + ring_bytes;
       }
-      // the tensor-core far history's part buffer (inline path; helpers reuse the space)
-      if (tc && smem + sizeof(double) * pf::TC_RED <= 227 * 1024) {
-        red_off = (int)smem;
-        smem += sizeof(double) * pf::TC_RED;
-      }
+      // split tensor-core helpers (sequential solver) keep their part buffer in this space
+      if (tc && hps > 1 && smem < sizeof(double) * pf::TC_RED) smem = sizeof(double) * pf::TC_RED;
       PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       PF_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
       int helpers = (c->allow_helpers && bs * (1 + hps) <= per_sm * c->num_sms) ? hps : 0;
@@ -347,11 +344,10 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
       int smem_total = (int)smem;
       if (helpers) {
         void* args[] = {(void*)&cl, (void*)&spp, (void*)&d_u, (void*)&nl, (void*)&nsl, (void*)&helpers,
-                        (void*)&ring_off, (void*)&smem_total, (void*)&red_off, (void*)&sync, (void*)&dp, (void*)&dout,
-                        (void*)&dst};
+                        (void*)&ring_off, (void*)&smem_total, (void*)&sync, (void*)&dp, (void*)&dout, (void*)&dst};
         PF_CUDA(c, cudaLaunchCooperativeKernel((void*)kern, dim3(ns * (1 + hps)), dim3(NT), args, smem, st));
       } else {
-        kern<<<ns, NT, smem, st>>>(cl, spp, d_u, nl, nsl, 0, ring_off, smem_total, red_off, sync, dp, dout, dst);
+        kern<<<ns, NT, smem, st>>>(cl, spp, d_u, nl, nsl, 0, ring_off, smem_total, sync, dp, dout, dst);
       }
       c->last_helpers = helpers;
     });

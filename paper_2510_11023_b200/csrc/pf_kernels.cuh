@@ -497,7 +497,7 @@ __device__ __forceinline__ void pf_jitter(int a, int b) {
 template <class SP, class SPP, int NT, int EPT>
 __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const double* __restrict__ U, int n_lo,
                                                    int nslices, int helpers, int ring_off, int smem_total,
-                                                   int red_off, SweepSync sync,
+                                                   SweepSync sync,
                                                    double* paths,
                                                    double* __restrict__ out, Status* __restrict__ status) {
   extern __shared__ __align__(16) char smem[];
