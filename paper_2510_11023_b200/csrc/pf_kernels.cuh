@@ -728,9 +728,10 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     x[i] = (e < c.size) ? srow[e] : 0.0;
     if (e < c.size) {
       path[e] = x[i];
-      if (ring) ring[e] = x[i];
+      if (EPT != 2 && ring) ring[e] = x[i];
     }
   }
+  if (EPT == 2 && ring) reinterpret_cast<double2*>(ring)[threadIdx.x] = make_double2(x[0], x[EPT - 1]);
   const double* hs = nullptr;
   int J = 0;
   double hnext[EPT], cnext[EPT];  // this block's far rows, prefetched one substep ahead
@@ -855,8 +856,33 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       if (r + 1 < tau_until && r + 1 <= c.m) wnext[j] = ext[(size_t)(r + 1) * 8 + j];
     }
     double h[EPT], ct[EPT], xg[EPT], xn[EPT];
+    // EPT = 2 (every size == 2 NT variant): the ring holds a thread's two entries
+    // side by side, one 16-byte load per row feeding both entries' chains; near
+    // weights from the parameter bank
+    if (EPT == 2 && ring) {
+      const double2* ring2 = reinterpret_cast<const double2*>(ring);
+      double a0 = hcur[0], a1 = hcur[EPT - 1], g0 = wcur[0] * x[0], g1 = wcur[0] * x[EPT - 1];
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) {
+      for (int q = 1; q < NR; ++q) {
+        const double2 vv = (r - q >= 0) ? ring2[((r - q) & (NR - 1)) * NT + threadIdx.x] : make_double2(0.0, 0.0);
+        if (r - q > J) {
+          a0 = fma(c.anear[q], vv.x, a0);
+          a1 = fma(c.anear[q], vv.y, a1);
+        }
+        if (q - 1 >= 1 && q - 1 <= EXT && q - 1 <= p) {  // guess weight j = q - 1 takes row r - 1 - j
+          g0 = fma(wcur[q - 1], vv.x, g0);
+          g1 = fma(wcur[q - 1], vv.y, g1);
+        }
+      }
+      h[0] = a0;
+      h[EPT - 1] = a1;
+      ct[0] = ccur[0];
+      ct[EPT - 1] = ccur[EPT - 1];
+      xg[0] = g0;
+      xg[EPT - 1] = g1;
+    }
+#pragma unroll
+    for (int i = 0; i < EPT && !(EPT == 2 && ring); ++i) {
       const int e = threadIdx.x + i * NT;
       double acc = 0.0, cb = 0.0, g = x[i];
       if (e < c.size) {
@@ -899,9 +925,11 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       x[i] = xn[i];
       if (e < c.size) {
         path[(size_t)r * c.size + e] = x[i];
-        if (ring) ring[(size_t)(r & (NR - 1)) * c.size + e] = x[i];
+        if (EPT != 2 && ring) ring[(size_t)(r & (NR - 1)) * c.size + e] = x[i];
       }
     }
+    if (EPT == 2 && ring)
+      reinterpret_cast<double2*>(ring)[(r & (NR - 1)) * NT + threadIdx.x] = make_double2(x[0], x[EPT - 1]);
   }
   if (st.code == ST_OK) {
 #pragma unroll
