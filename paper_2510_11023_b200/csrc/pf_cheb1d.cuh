@@ -38,7 +38,7 @@ struct Cheb1D {
   }
   static size_t smem_bytes(int degree) {
     const size_t npts = degree + 1, ni = degree - 1, ld = ld_of((int)ni);
-    return sizeof(double) * (npts * npts + 2 * npts + ni * ld + 3 * npts + ni + 4 + RED_DOUBLES) + sizeof(int) * (ni + 4);
+    return sizeof(double) * (npts * npts + 2 * npts + ni * ld + 3 * npts + ni + 5 + RED_DOUBLES) + sizeof(int) * (ni + 4);
   }
 
   __device__ void init(char* smem, const Cheb1DParams& p) {
@@ -55,6 +55,7 @@ struct Cheb1D {
     xs = dv + npts;
     pivs = xs + npts;
     double* rs = pivs + 4;
+    if (reinterpret_cast<uintptr_t>(rs) & 15) rs += 1;  // the reducer reads its slots as 16-byte pairs
     red.init(rs);
     perm = reinterpret_cast<int*>(rs + RED_DOUBLES);
     for (int i = threadIdx.x; i < npts * npts; i += NT) d1s[i] = p.d1[i];

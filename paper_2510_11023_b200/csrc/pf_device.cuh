@@ -164,8 +164,9 @@ struct Reducer {
     double sa = 0.0, sb = 0.0;
 #pragma unroll
     for (int i = 0; i < NT / 32; ++i) {
-      sa += slot[4 * i];
-      sb += slot[4 * i + 1];
+      const double2 v = reinterpret_cast<const double2*>(slot)[2 * i];  // slot[4i], slot[4i+1]
+      sa += v.x;
+      sb += v.y;
     }
     buf ^= 1;
     return make_double2(sa, sb);
@@ -223,10 +224,12 @@ struct Reducer {
     double sa = 0.0, sb = 0.0, sc = 0.0, sd = 0.0;
 #pragma unroll
     for (int i = 0; i < NT / 32; ++i) {
-      sa += slot[4 * i];
-      sb += slot[4 * i + 1];
-      sc += slot[4 * i + 2];
-      sd += slot[4 * i + 3];
+      const double2 v = reinterpret_cast<const double2*>(slot)[2 * i];
+      const double2 u = reinterpret_cast<const double2*>(slot)[2 * i + 1];
+      sa += v.x;
+      sb += v.y;
+      sc += u.x;
+      sd += u.y;
     }
     buf ^= 1;
     return make_double4(sa, sb, sc, sd);

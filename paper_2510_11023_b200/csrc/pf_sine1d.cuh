@@ -377,6 +377,10 @@ struct Sine1D {
   Reducer<NT> red;
   double tol2;
   int maxit;
+  // phase factors of the owned modes, ph[k] and ph[Q-k], kept in registers (every
+  // synthesis input and analysis gather of every substep reads them)
+  static constexpr bool kPhReg = EPT <= 2;  // (EPT = 4 would spill)
+  cd phk[EPT], phq[EPT];
 
   static size_t smem_bytes() { return sizeof(cd) * (TW + 3 * Q) + sizeof(double) * (4 * Q + RED_DOUBLES); }
 
@@ -401,6 +405,12 @@ struct Sine1D {
     ph = phs;
     tol2 = p.pcg_tol * p.pcg_tol;
     maxit = p.pcg_maxit;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int k = 1 + (int)threadIdx.x + i * NT;
+      phk[i] = (kPhReg && k <= M) ? p.ph[k] : cd{0.0, 0.0};
+      phq[i] = (kPhReg && k <= M) ? p.ph[Q - k] : cd{0.0, 0.0};
+    }
     __syncthreads();
   }
 
@@ -425,7 +435,7 @@ struct Sine1D {
     for (int i = 0; i < EPT; ++i) {
       const int k = mode(i);
       if (k < M) {
-        const cd p = ph[k], pq = ph[Q - k];
+        const cd p = kPhReg ? phk[i] : ph[k], pq = kPhReg ? phq[i] : ph[Q - k];
         // V1_k = -i p a, V2_k = p b  -> W_k = V1 + i V2
         const double a = av[i], b = bv[i];
         const cd v1 = {p.y * a, -p.x * a};
@@ -436,7 +446,7 @@ struct Sine1D {
         const cd u2 = {pq.y * b, -pq.x * b};
         A[S(Q - k)] = {u1.x - u2.y, u1.y + u2.x};
       } else if (k == M) {
-        const cd p = ph[M];
+        const cd p = kPhReg ? phk[i] : ph[M];
         const double a = av[i], b = bv[i];
         const cd v1 = {p.x * a + p.y * a, p.y * a - p.x * a};  // p (a - i a)
         const cd v2 = {p.x * b + p.y * b, p.y * b - p.x * b};  // p (b - i b)
@@ -508,7 +518,7 @@ struct Sine1D {
       const int k = mode(i);
       kp[i] = 0.0;
       if (k <= M) {
-        const cd a = Z[S(k)], b = Z[S(Q - k)], c = ph[k];
+        const cd a = Z[S(k)], b = Z[S(Q - k)], c = kPhReg ? phk[i] : ph[k];
         const double Dx = a.x - b.x, Dy = a.y + b.y;
         kp[i] = SQ2 * CUDART_PI * (double)k * (0.5 * (c.x * Dy - c.y * Dx));
       }
@@ -658,7 +668,7 @@ struct Sine1D {
       const int k = mode(i);
       x[i] = r[i] = 0.0;
       if (k <= M) {
-        const cd a = Z[S(k)], b = Z[S(Q - k)], c = ph[k], c2 = ph[Q - k];
+        const cd a = Z[S(k)], b = Z[S(Q - k)], c = kPhReg ? phk[i] : ph[k], c2 = kPhReg ? phq[i] : ph[Q - k];
         const double Dx = a.x - b.x, Dy = a.y + b.y;
         const double X2 = 0.5 * (c.x * Dy - c.y * Dx);
         const double X1 = 0.5 * (c2.x * (b.x + a.x) + c2.y * (b.y - a.y));
