@@ -272,7 +272,8 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   // per slice: block tiles [parity][hps + 1][2][HB][size] (+ the split tensor-core
   // helpers' part tiles [parity][batch][part][512], k_fine_sweep)
   const bool tc = c->kind == PF_SPACE_SINE1D && c->lgQ >= 10 && c->size % pf::TC_BATCH == 0;
-  const size_t parts_len = (tc && hps > 1) ? (size_t)2 * (c->size / pf::TC_BATCH) * 8 * 512 : 0;
+  const size_t parts_len =
+      (tc && hps > 1) ? (size_t)2 * (c->size / pf::TC_BATCH) * pf::tc_parts(hps, c->size / pf::TC_BATCH) * 512 : 0;
   // far history of one-helper sweeps: measured at config 3 (profiles/r02_far_history_variants.txt)
   // DFMA register tiles 8.8 ms, DMMA with direct loads 13.1 ms, DMMA + TMA bulk copies 10.1 ms
   // per sweep: the DFMA tiles stay the default; PF_FAR_TC=1/2 select the others
@@ -993,7 +994,9 @@ int pf_fine_sequential(pf_ctx* c, const double* u0, double* states) {
   if (c->io.ensure((size_t)2 * c->size)) return cuda_fail(c, cudaErrorMemoryAllocation, "io");
   if (upload(c, c->io.p, u0, c->size)) return c->err.code;
   if (ensure_status(c, 1)) return c->err.code;
-  const int hps = (int)std::max<long>(1, std::min<long>(c->num_sms - 1, total / 1024));
+  // far-history helpers: one per 1024 substeps up to the SMs left over (config 3:
+  // 128 = 8 batches x 16 parts of the tensor-core split)
+  const int hps = (int)std::max<long>(1, std::min<long>(std::min<long>(c->num_sms - 1, 128), total / 512));
   int rc = launch_fine(c, c->io.p, 0, 1, c->io.p + c->size, c->d_status, (int)total, hps);
   if (rc == PF_ERR_UNSUPPORTED) rc = launch_fine(c, c->io.p, 0, 1, c->io.p + c->size, c->d_status, (int)total, 1);
   if (rc) return rc;

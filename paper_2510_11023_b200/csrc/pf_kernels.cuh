@@ -284,6 +284,8 @@ struct SweepSync {
 // (tested against the inline path to 1e-12 and against the oracle).
 // ---------------------------------------------------------------------------
 constexpr int TC_BATCH = 64;          // modes per batch (8 groups of 8)
+// parts per batch of the split helpers: 8, or 16 when there are helpers for it
+__host__ __device__ constexpr int tc_parts(int hps, int nb) { return hps >= 16 * nb ? 16 : 8; }
 constexpr int TC_RED = 8 * 8 * 64;    // doubles of the per-CTA part buffer (8 warps x 8 groups x 64)
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
@@ -521,7 +523,9 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   const int NB = c.size / TC_BATCH;
   // far history on the FP64 tensor cores: split helpers always, else when selected
   const bool tc = NT == 256 && c.size % TC_BATCH == 0 && (hps > 1 || c.far_tc > 0);
-  const size_t parts_len = (tc && hps > 1) ? (size_t)2 * NB * 8 * 512 : 0;
+  // split helpers: each 64-mode batch's k-steps in PK interleaved parts, one (batch, part) unit per helper round
+  const int PK = tc_parts(hps, NB);
+  const size_t parts_len = (tc && hps > 1) ? (size_t)2 * NB * PK * 512 : 0;
   double* scr = c.scratch + (size_t)b * ((size_t)2 * (hps + 1) * 2 * HB * c.size + parts_len);
   auto slot = [&](int parity, int h) { return scr + ((size_t)parity * (hps + 1) + h) * 2 * HB * c.size; };
   double* parts = scr + (size_t)2 * (hps + 1) * 2 * HB * c.size;
@@ -586,13 +590,13 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         PF_TH(12);
         cta_publish_add(sync.ready + (size_t)b * hps, NB);
       } else {  // split helpers (sequential solver): unit (batch, part) -> helper unit mod hps
-        for (int u = hid; u < NB * 8; u += hps) {
-          const int batch = u >> 3, part = u & 7;
+        for (int u = hid; u < NB * PK; u += hps) {
+          const int batch = u / PK, part = u % PK;
           double acc[8][2];
-          tc_far_part(path, c.size, aw, R0, J, batch, part + 8 * w, 64, acc);
+          tc_far_part(path, c.size, aw, R0, J, batch, part + PK * w, 8 * PK, acc);
           tc_store_part(red, acc);
           __syncthreads();
-          double* pb = parts + (((size_t)(beta & 1) * NB + batch) * 8 + part) * 512;
+          double* pb = parts + (((size_t)(beta & 1) * NB + batch) * PK + part) * 512;
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             const int sl = 2 * (int)threadIdx.x + i;
@@ -601,8 +605,8 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
             for (int ww = 1; ww < 8; ++ww) sum += red[(size_t)ww * 512 + sl];
             pb[sl] = sum;
           }
-          if (cta_last_arrival(sync.tickets + (size_t)b * 64 + (beta & 1) * 32 + batch, 8)) {
-            const double* p0 = parts + ((size_t)(beta & 1) * NB + batch) * 8 * 512;
+          if (cta_last_arrival(sync.tickets + (size_t)b * 64 + (beta & 1) * 32 + batch, PK)) {
+            const double* p0 = parts + ((size_t)(beta & 1) * NB + batch) * PK * 512;
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
               int sl, rr, col;
@@ -610,7 +614,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
               const int e = TC_BATCH * batch + col;
               double sum = __ldcg(p0 + sl);
 #pragma unroll
-              for (int pp = 1; pp < 8; ++pp) sum += __ldcg(p0 + (size_t)pp * 512 + sl);
+              for (int pp = 1; pp < PK; ++pp) sum += __ldcg(p0 + (size_t)pp * 512 + sl);
               hs[(size_t)rr * c.size + e] = c.bfine[R0 + rr] * __ldcg(row0 + e) + sum;
             }
             cta_publish_add(sync.ready + (size_t)b * hps, 1);

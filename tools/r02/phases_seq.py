@@ -23,3 +23,5 @@ print(f"run_fine_sequential N={N}: {t1 - t0:.3f} s")
 for k in range(16):
     if buf[k]:
         print(f"{names.get(k, k):28s} {buf[k]/N:10.0f} cyc/substep  {100*buf[k]/tot:5.1f}%")
+st = _lib.context_for(prob, op, g).stats()
+print("pcg iterations per solve", st["pcg_iterations"] / max(st["solves"], 1), st)
