@@ -133,6 +133,9 @@ int pf_set_stream(pf_ctx* ctx, void* stream);
 const char* pf_version(void);
 /* development aid: per-phase cycle counters of slice 0 (zeros unless built with -DPF_PHASE_TIMING) */
 int pf_debug_phases(long long* out16, int reset);
+/* development aid: per-warp clock64 timeline of 8 substeps of one slice CTA, out[8 warps][8 substeps][64
+   points] (zeros unless built with -DPF_TRACE; tools/r02/trace.py) */
+int pf_debug_trace(long long* out4096);
 /* development aid: entry/exit times (GPU globaltimer, ns) of each slice of the last 1-D fine
    sweep, out[2i] = entry, out[2i+1] = exit (load-balance diagnostic, tools/slice_finish.py) */
 int pf_debug_slice_times_ns(const pf_ctx* ctx, long long* out, int n);

@@ -191,6 +191,16 @@ pf::Cheb1DParams cheb_params(const pf_ctx* c) {
 }
 
 // Dispatch: binds SP (space type), SPP (its params), NT, EPT and `spp`.
+#ifdef PF_ONLY_S10  // experiment builds (tools/): the config-3 variant only, a quarter of the compile time
+#define PF_DISPATCH(ctx, ...) \
+  switch ((ctx)->variant) { \
+    case V_S10: { using SP = pf::Sine1D<256, 2, 10>; using SPP = pf::Sine1DParams; \
+      constexpr int NT = 256, EPT = 2; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
+    default: \
+      return set_error(ctx, PF_ERR_UNSUPPORTED, "no kernel variant"); \
+  }
+
+#else
 #define PF_DISPATCH(ctx, ...) \
   switch ((ctx)->variant) { \
     case V_S2: { using SP = pf::Sine1D<32, 1, 2>; using SPP = pf::Sine1DParams; \
@@ -218,6 +228,7 @@ pf::Cheb1DParams cheb_params(const pf_ctx* c) {
     default: \
       return set_error(ctx, PF_ERR_UNSUPPORTED, "no kernel variant"); \
   }
+#endif
 
 int ensure_status(pf_ctx* c, int n) {
   if (n <= c->status_cap) return 0;
@@ -525,6 +536,17 @@ int pf_debug_phases(long long* out16, int reset) {
 #else
   for (int i = 0; i < 16; ++i) out16[i] = 0;
   (void)reset;
+#endif
+  return PF_OK;
+}
+
+// Per-warp timeline of the traced substeps (only in -DPF_TRACE builds): out[8 warps][8 substeps][64 points].
+int pf_debug_trace(long long* out4096) {
+#ifdef PF_TRACE
+  if (cudaMemcpyFromSymbol(out4096, pf::g_trace, sizeof(long long) * 8 * pf::TR_STEPS * pf::TR_POINTS) != cudaSuccess)
+    return PF_ERR_CUDA;
+#else
+  for (int i = 0; i < 4096; ++i) out4096[i] = 0;
 #endif
   return PF_OK;
 }

@@ -42,6 +42,29 @@ __device__ long long g_phase_last_h;
   } while (0)
 #endif
 
+// Optional per-warp timeline of a few substeps of one slice CTA (build with
+// -DPF_TRACE; read with pf_debug_trace).  Lane 0 of every warp stores clock64()
+// at each trace point: unlike the thread-0 phase timers above this shows every
+// warp's arrival at every barrier.  Compiled out of the product library.
+#ifdef PF_TRACE
+#ifndef PF_TRACE_SLICE
+#define PF_TRACE_SLICE 1
+#endif
+#ifndef PF_TRACE_R0
+#define PF_TRACE_R0 513
+#endif
+constexpr int TR_STEPS = 8, TR_POINTS = 64;
+__device__ long long g_trace[8][TR_STEPS][TR_POINTS];
+#define PF_TR(tr, id)                                                                   \
+  do {                                                                                  \
+    if ((tr) >= 0 && (threadIdx.x & 31) == 0) g_trace[threadIdx.x >> 5][(tr)][(id)] = clock64(); \
+  } while (0)
+#else
+#define PF_TR(tr, id) \
+  do {                \
+  } while (0)
+#endif
+
 struct cd {
   double x, y;
 };
@@ -61,6 +84,52 @@ __device__ __forceinline__ void dft4(cd& a0, cd& a1, cd& a2, cd& a3) {
   a1 = INV ? csub(t1, mi3) : cadd(t1, mi3);
   a2 = csub(t0, t2);
   a3 = INV ? cadd(t1, mi3) : csub(t1, mi3);
+}
+
+// ---------------------------------------------------------------------------
+// fast FP64 scalars for the latency-bound substep chain (branch-free, so the
+// compiler interleaves the independent evaluations of a thread)
+// ---------------------------------------------------------------------------
+// 1/a for normal a (no zero / inf / denormal handling): MUFU.RCP64H seed (~20 bits)
+// + two Newton steps, <= 1 ulp.  The callers' operands are sums of positive terms.
+__device__ __forceinline__ double rcp_fast(double a) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  double e = fma(-a, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-a, y, 1.0);
+  return fma(y, e, y);
+}
+
+// tanh(u) to ~2e-16 ABSOLUTE error (not relative: for D = 1.5 + 0.5 tanh(u) the
+// absolute error is what reaches the coefficient, at its rounding level):
+// 1 - 2 / (exp(2|u|) + 1), exp by range reduction to |r| <= ln2/2 and a degree-12
+// Taylor polynomial, no branches (CUDA's tanh has a small-|u| branch that diverges
+// across a slice's grid points and serialises a thread's four evaluations).
+__device__ __forceinline__ double tanh_abs(double u) {
+  const double x = fmin(2.0 * fabs(u), 80.0);
+  const double kd = fma(x, 1.4426950408889634, 6755399441055744.0);  // 1.5 * 2^52: round to nearest integer
+  const int k = __double2loint(kd);
+  const double n = kd - 6755399441055744.0;
+  double r = fma(n, -6.93147180369123816490e-01, x);  // ln2 hi
+  r = fma(n, -1.90821492927058770002e-10, r);          // ln2 lo
+  double p = 1.0 / 479001600.0;
+  p = fma(p, r, 1.0 / 39916800.0);
+  p = fma(p, r, 1.0 / 3628800.0);
+  p = fma(p, r, 1.0 / 362880.0);
+  p = fma(p, r, 1.0 / 40320.0);
+  p = fma(p, r, 1.0 / 5040.0);
+  p = fma(p, r, 1.0 / 720.0);
+  p = fma(p, r, 1.0 / 120.0);
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);  // exp(r)
+  // exp(x) = p * 2^k, k in [0, 116]: add k to the exponent field
+  const double e = __hiloint2double(__double2hiint(p) + (k << 20), __double2loint(p));
+  const double t = fma(-2.0, rcp_fast(e + 1.0), 1.0);
+  return copysign(t, u);
 }
 
 // ---------------------------------------------------------------------------
@@ -96,7 +165,7 @@ __device__ __forceinline__ double fn_D(const Fn& f, double x, double x2, double 
       return 1.0 + u2 / (1.0 + u2);
     }
     case 3:  // PF_FN_CFG3
-      return 1.5 + 0.5 * tanh(u);
+      return 1.5 + 0.5 * tanh_abs(u);
     case 4: {  // PF_FN_CFG45
       const double s = sin(u);
       return (1.0 + 0.5 * x) * (1.0 + 0.5 * (s * s));
@@ -161,15 +230,19 @@ struct Reducer {
       slot[4 * w + 1] = b;
     }
     __syncthreads();
-    double sa = 0.0, sb = 0.0;
+    // pairwise (fixed-shape) tree over the warps' partials: log2(NT/32) dependent adds
+    double2 v[NT / 32];
 #pragma unroll
-    for (int i = 0; i < NT / 32; ++i) {
-      const double2 v = reinterpret_cast<const double2*>(slot)[2 * i];  // slot[4i], slot[4i+1]
-      sa += v.x;
-      sb += v.y;
-    }
+    for (int i = 0; i < NT / 32; ++i) v[i] = reinterpret_cast<const double2*>(slot)[2 * i];  // slot[4i], slot[4i+1]
+#pragma unroll
+    for (int w2 = NT / 64; w2 > 0; w2 >>= 1)
+#pragma unroll
+      for (int i = 0; i < w2; ++i) {
+        v[i].x += v[i + w2].x;
+        v[i].y += v[i + w2].y;
+      }
     buf ^= 1;
-    return make_double2(sa, sb);
+    return v[0];
   }
   __device__ __forceinline__ double3 sum3(double a, double b, double c) {
 #pragma unroll
@@ -221,18 +294,23 @@ struct Reducer {
       slot[4 * w + 3] = d;
     }
     __syncthreads();
-    double sa = 0.0, sb = 0.0, sc = 0.0, sd = 0.0;
+    double2 v[NT / 32], u[NT / 32];
 #pragma unroll
     for (int i = 0; i < NT / 32; ++i) {
-      const double2 v = reinterpret_cast<const double2*>(slot)[2 * i];
-      const double2 u = reinterpret_cast<const double2*>(slot)[2 * i + 1];
-      sa += v.x;
-      sb += v.y;
-      sc += u.x;
-      sd += u.y;
+      v[i] = reinterpret_cast<const double2*>(slot)[2 * i];
+      u[i] = reinterpret_cast<const double2*>(slot)[2 * i + 1];
     }
+#pragma unroll
+    for (int w2 = NT / 64; w2 > 0; w2 >>= 1)
+#pragma unroll
+      for (int i = 0; i < w2; ++i) {
+        v[i].x += v[i + w2].x;
+        v[i].y += v[i + w2].y;
+        u[i].x += u[i + w2].x;
+        u[i].y += u[i + w2].y;
+      }
     buf ^= 1;
-    return make_double4(sa, sb, sc, sd);
+    return make_double4(v[0].x, v[0].y, u[0].x, u[0].y);
   }
   __device__ __forceinline__ double sum(double a) { return sum2(a, 0.0).x; }
   __device__ __forceinline__ double max(double a) {

@@ -766,6 +766,10 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     const double t = (double)n * c.dT + (double)(r - 1) * c.dt;
     const int rr = (r - 1) % HB;
     const int beta = (r - 1) / HB;
+#ifdef PF_TRACE
+    sp.tr = ((int)blockIdx.x == PF_TRACE_SLICE && r >= PF_TRACE_R0 && r < PF_TRACE_R0 + TR_STEPS) ? r - PF_TRACE_R0 : -1;
+#endif
+    PF_TR(sp.tr, 0);
     PF_T(10);
     if (c.cancel && rr == 0 && beta > 0 &&
         __syncthreads_or(threadIdx.x == 0 && *(volatile const int*)c.cancel != 0)) {
@@ -829,6 +833,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
         hnext[i] = (e < c.size) ? __ldcg(hs + e) : 0.0;
       }
     }
+    PF_TR(sp.tr, 1);
     PF_T(8);
     double hcur[EPT], ccur[EPT];
 #pragma unroll
@@ -916,6 +921,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       ct[i] = cb;
       xg[i] = g;
     }
+    PF_TR(sp.tr, 2);
     PF_T(9);
     const int code = sp.step(c.fn, x, xg, t, c.gam_f, h, ct, xn, st);
     if (code != ST_OK) {
@@ -934,6 +940,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     }
     if (EPT == 2 && ring)
       reinterpret_cast<double2*>(ring)[(r & (NR - 1)) * NT + threadIdx.x] = make_double2(x[0], x[EPT - 1]);
+    PF_TR(sp.tr, 47);
   }
   if (st.code == ST_OK) {
 #pragma unroll

@@ -339,25 +339,32 @@ __device__ __forceinline__ void first_fwd10(cd (&x)[4], cd* __restrict__ b) {
   b[sw10(4 * j + 3)] = x[3];
 }
 
+// (tr, id0: PF_TRACE timeline slot of the first pass; no code in the product build)
 template <int NT>
-__device__ __forceinline__ cd* inv_passes10(cd* A, cd* B, const cd* tw) {
+__device__ __forceinline__ cd* inv_passes10(cd* A, cd* B, const cd* tw, int tr = -1, int id0 = 0) {
   r8_pass10<true, 1, 0>(A, B, tw);
   bar<NT>();
+  PF_TR(tr, id0);
   r8_pass10<true, 8, T10_R8_8>(B, A, tw);
   bar<NT>();
+  PF_TR(tr, id0 + 1);
   r4_pass10<true, 64, T10_R4_64>(A, B, tw);
   bar<NT>();
+  PF_TR(tr, id0 + 2);
   return B;
 }
 
 template <int NT>
-__device__ __forceinline__ cd* fwd_passes10(cd* Y, cd* X, const cd* tw) {
+__device__ __forceinline__ cd* fwd_passes10(cd* Y, cd* X, const cd* tw, int tr = -1, int id0 = 0) {
   r4_pass10<false, 4, T10_R4_4>(Y, X, tw);
   bar<NT>();
+  PF_TR(tr, id0);
   r8_pass10<false, 16, T10_R8_16>(X, Y, tw);
   bar<NT>();
+  PF_TR(tr, id0 + 1);
   r8_pass10<false, 128, T10_R8_128>(Y, X, tw);
   bar<NT>();
+  PF_TR(tr, id0 + 2);
   return X;
 }
 
@@ -381,6 +388,7 @@ struct Sine1D {
   // synthesis input and analysis gather of every substep reads them)
   static constexpr bool kPhReg = EPT <= 2;  // (EPT = 4 would spill)
   cd phk[EPT], phq[EPT];
+  int tr = -1;  // PF_TRACE timeline row of the current substep (-1: not traced)
 
   static size_t smem_bytes() { return sizeof(cd) * (TW + 3 * Q) + sizeof(double) * (4 * Q + RED_DOUBLES); }
 
@@ -466,7 +474,7 @@ struct Sine1D {
   }
 
   // K p for owned modes (p, Kp in registers)
-  __device__ __forceinline__ void apply_k(const double* p, double* kp) {
+  __device__ __forceinline__ void apply_k(const double* p, double* kp, int id0 = 0) {
     double av[EPT], bv[EPT];
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
@@ -475,9 +483,10 @@ struct Sine1D {
     }
     synth_input(av, bv);
     bar<NT>();
+    PF_TR(tr, id0);
     cd* Z;
     if constexpr (LG == 10 && NT == 256) {
-      cd* X = inv_passes10<NT>(A, B, twp);
+      cd* X = inv_passes10<NT>(A, B, twp, tr, id0 + 1);
       cd* Y = (X == A) ? B : A;
       cd v[4];
       last_inv10(X, twp, v);
@@ -485,7 +494,8 @@ struct Sine1D {
       for (int r = 0; r < 4; ++r) v[r] = {0.0, dq[qof(threadIdx.x, r)] * (0.5 * v[r].y)};
       first_fwd10(v, Y);
       bar<NT>();
-      Z = fwd_passes10<NT>(Y, X, twp);
+      PF_TR(tr, id0 + 4);
+      Z = fwd_passes10<NT>(Y, X, twp, tr, id0 + 5);
     } else if constexpr (kFuse) {
       constexpr int P = LG / 2;
       cd* X = fft_passes<LG, NT, true, 0, P - 1>(A, B, twp);
@@ -597,7 +607,15 @@ struct Sine1D {
       synth_input(av, bv);
     }
     bar<NT>();
-    const double emt = fn.id == 1 ? exp(-t) : 0.0;  // only PF_FN_POLY's source uses exp(-t)
+    PF_TR(tr, 3);
+    // only PF_FN_POLY's source uses exp(-t): behind a real branch (as a select the
+    // compiler evaluated exp() in every substep of every functor, ~110 FP64-pipe
+    // instructions per warp)
+    double emt = 0.0;
+    if (fn.id == 1) {
+      emt = exp(-t);
+      asm volatile("" : "+d"(emt));
+    }
     double dsum = 0.0, nbad = 0.0;
     int bad = 0x7fffffff;
     cd* Z;
@@ -606,7 +624,7 @@ struct Sine1D {
     // one block reduction fewer per substep (the FFT itself does not depend
     // on them; a non-finite D is reported before any solve)
     if constexpr (LG == 10 && NT == 256) {
-      cd* X = inv_passes10<NT>(A, B, twp);
+      cd* X = inv_passes10<NT>(A, B, twp, tr, 4);
       cd* Y = (X == A) ? B : A;
       PF_T(1);
       cd v[4];
@@ -620,8 +638,9 @@ struct Sine1D {
       }
       first_fwd10(v, Y);
       bar<NT>();
+      PF_TR(tr, 7);
       PF_T(2);
-      Z = fwd_passes10<NT>(Y, X, twp);
+      Z = fwd_passes10<NT>(Y, X, twp, tr, 8);
     } else if constexpr (kFuse) {
       constexpr int P = LG / 2;
       cd* X = fft_passes<LG, NT, true, 0, P - 1>(A, B, twp);
@@ -681,7 +700,9 @@ struct Sine1D {
         rr = fma(r[i], r[i], rr);
       }
     }
+    PF_TR(tr, 11);
     const double4 s0 = red.sum4(dsum, nbad, bb, rr);
+    PF_TR(tr, 12);
     PF_T(4);
     if (s0.y > 0.0) {
       st.node = red.min_int(bad);
@@ -695,7 +716,8 @@ struct Sine1D {
       p[i] = z[i] = pinv[i] = 0.0;
       if (k <= M) {
         const double kk = (double)k;
-        pinv[i] = 1.0 / (1.0 + gam * dbar * (CUDART_PI * CUDART_PI) * (kk * kk));
+        // (a preconditioner entry: rcp_fast's <= 1 ulp is as good as the division)
+        pinv[i] = rcp_fast(1.0 + gam * dbar * (CUDART_PI * CUDART_PI) * (kk * kk));
         z[i] = pinv[i] * r[i];
         p[i] = z[i];
         rzl = fma(r[i], z[i], rzl);
@@ -712,12 +734,14 @@ struct Sine1D {
     const double thr = tol2 * s0.z;
     double rrv = s0.w;
     int it = 0;
+    PF_TR(tr, 13);
     if (rrv > thr) {
       double rz = 0.0;  // (r0, z0): reduced with the first iteration's (p, q)
       for (it = 1; it <= maxit; ++it) {
         double kp[EPT], qv[EPT];
         PF_T(6);
-        apply_k(p, kp);
+        const int tb = it <= 2 ? 14 + (it - 1) * 16 : 62;
+        apply_k(p, kp, tb);
         PF_T(5);
         double pql = 0.0;
 #pragma unroll
@@ -725,10 +749,15 @@ struct Sine1D {
           qv[i] = p[i] + gam * kp[i];
           pql = fma(p[i], qv[i], pql);
         }
+        PF_TR(it <= 2 ? tr : -1, tb + 8);
         const double2 pr = red.sum2(pql, it == 1 ? rzl : 0.0);
+        PF_TR(it <= 2 ? tr : -1, tb + 9);
         const double pq = pr.x;
         if (it == 1) rz = pr.y;
-        const double alpha = rz / pq;
+        // alpha, beta through rcp_fast (the division's latency sits on every iteration's
+        // critical path; x and r are updated with the same alpha, so CG stays consistent);
+        // a zero or non-finite (p, A p) gives a non-finite alpha either way
+        const double alpha = rz * rcp_fast(pq);
         if (!isfinite(alpha)) return ST_SOLVER;
         double rrl = 0.0, rzn = 0.0;
 #pragma unroll
@@ -739,11 +768,13 @@ struct Sine1D {
           rrl = fma(r[i], r[i], rrl);
           rzn = fma(r[i], z[i], rzn);
         }
+        PF_TR(it <= 2 ? tr : -1, tb + 10);
         const double2 s = red.sum2(rrl, rzn);
+        PF_TR(it <= 2 ? tr : -1, tb + 11);
         rrv = s.x;
         if (!isfinite(rrv)) return ST_SOLVER;
         if (!(rrv > thr)) break;  // converged
-        const double beta = s.y / rz;
+        const double beta = s.y * rcp_fast(rz);
         rz = s.y;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) p[i] = fma(beta, p[i], z[i]);
@@ -754,6 +785,7 @@ struct Sine1D {
     // x = x0 + sum(alpha p) with finite alpha, p and a finite guess: finite
 #pragma unroll
     for (int i = 0; i < EPT; ++i) xout[i] = x[i];
+    PF_TR(tr, 46);
     PF_T(7);
     return ST_OK;
   }
