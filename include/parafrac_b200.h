@@ -136,6 +136,8 @@ int pf_debug_phases(long long* out16, int reset);
 /* development aid: per-warp clock64 timeline of 8 substeps of one slice CTA, out[8 warps][8 substeps][64
    points] (zeros unless built with -DPF_TRACE; tools/r02/trace.py) */
 int pf_debug_trace(long long* out4096);
+/* development aid: clock64 at the loop top of substeps 0..n-1 (n <= 4096) of the traced slice (-DPF_TRACE) */
+int pf_debug_looptop(long long* out, int n);
 /* development aid: entry/exit times (GPU globaltimer, ns) of each slice of the last 1-D fine
    sweep, out[2i] = entry, out[2i+1] = exit (load-balance diagnostic, tools/slice_finish.py) */
 int pf_debug_slice_times_ns(const pf_ctx* ctx, long long* out, int n);

@@ -76,6 +76,7 @@ SIGNATURES = {
     "pf_version": (C.c_char_p, []),
     "pf_debug_phases": (C.c_int, [C.POINTER(C.c_longlong), C.c_int]),
     "pf_debug_trace": (C.c_int, [C.POINTER(C.c_longlong)]),
+    "pf_debug_looptop": (C.c_int, [C.POINTER(C.c_longlong), C.c_int]),
     "pf_debug_slice_times_ns": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong), C.c_int]),
     "pf_coarse_step": (C.c_int, [C.c_void_p, _dp, C.c_int, C.c_int, _dp]),
     "pf_run_coarse": (C.c_int, [C.c_void_p, _dp, _dp]),

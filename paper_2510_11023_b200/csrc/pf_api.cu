@@ -284,11 +284,16 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   // helpers' part tiles [parity][batch][part][512], k_fine_sweep)
   const bool tc = c->kind == PF_SPACE_SINE1D && c->lgQ >= 10 && c->size % pf::TC_BATCH == 0;
   const size_t parts_len =
-      (tc && hps > 1) ? (size_t)2 * (c->size / pf::TC_BATCH) * pf::tc_parts(hps, c->size / pf::TC_BATCH) * 512 : 0;
-  // far history of one-helper sweeps: measured at config 3 (profiles/r02_far_history_variants.txt)
-  // DFMA register tiles 8.8 ms, DMMA with direct loads 13.1 ms, DMMA + TMA bulk copies 10.1 ms
-  // per sweep: the DFMA tiles stay the default; PF_FAR_TC=1/2 select the others
-  int far_tc = 0;
+      (tc && hps > 1) ? (size_t)2 * (c->size / pf::TC_BATCH) * pf::tc_parts(hps, c->size / pf::TC_BATCH) * 512
+      : tc            ? (size_t)2 * pf::TC_G * pf::HB * c->size
+                      : 0;
+  // far history of one-helper sweeps (PF_FAR_TC): 0 DFMA register tiles, 1 DMMA with direct
+  // loads, 2 DMMA fed by TMA bulk copies with the old rows accumulated for four tiles per pass
+  // (pf_kernels.cuh TC_G).  Late in a config-3 sweep every helper re-reads its slice's whole path
+  // once per block -- 269 MB per block period, more than HBM delivers -- and engines 0 and 1 made
+  // the slice CTAs wait from block ~88 of 128 on; engine 2 reads a quarter of that and is the
+  // default where its one-warp-per-batch layout applies (M = 512).
+  int far_tc = (tc && c->size / pf::TC_BATCH <= 8) ? 2 : 0;
   if (const char* ft = std::getenv("PF_FAR_TC")) far_tc = (ft[0] == '1') ? 1 : (ft[0] == '2') ? 2 : 0;
   const size_t scr_stride = (size_t)2 * (hps + 1) * 2 * pf::HB * c->size + parts_len;
   if (c->scratch.ensure((size_t)cap * scr_stride)) return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
@@ -345,6 +350,10 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
       if (base + ring_bytes <= 227 * 1024) {
         ring_off = (int)base;
         smem = base + ring_bytes;
+      }
+      if (SP::kSide) {  // + the side warps' prepared rows [h' | guess'][NT] (16 bytes each)
+        if (ring_off < 0) return set_error(c, PF_ERR_UNSUPPORTED, "the state ring must fit at this size");
+        smem += 2 * 16 * (size_t)NT;
       }
       // split tensor-core helpers (sequential solver) keep their part buffer in this space
       if (tc && hps > 1 && smem < sizeof(double) * pf::TC_RED) smem = sizeof(double) * pf::TC_RED;
@@ -547,6 +556,17 @@ int pf_debug_trace(long long* out4096) {
     return PF_ERR_CUDA;
 #else
   for (int i = 0; i < 4096; ++i) out4096[i] = 0;
+#endif
+  return PF_OK;
+}
+
+// clock64 at the loop top of substeps 0..n-1 of the traced slice (only in -DPF_TRACE builds).
+int pf_debug_looptop(long long* out, int n) {
+#ifdef PF_TRACE
+  if (n < 0 || n > 4096) return PF_ERR_ARGUMENT;
+  if (cudaMemcpyFromSymbol(out, pf::g_looptop, sizeof(long long) * n) != cudaSuccess) return PF_ERR_CUDA;
+#else
+  for (int i = 0; i < n; ++i) out[i] = 0;
 #endif
   return PF_OK;
 }

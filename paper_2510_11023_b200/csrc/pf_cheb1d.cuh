@@ -22,6 +22,8 @@ struct Cheb1DParams {
 
 template <int NT, int EPT>
 struct Cheb1D {
+  static constexpr bool kSide = false;  // no idle-warp side work in this space (see Sine1D::kSide)
+  int tr = -1;                          // PF_TRACE timeline row (unused here)
   int npts, ni, LD;
   const double* d1;
   const double* nodes;

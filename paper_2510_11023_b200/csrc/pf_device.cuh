@@ -55,6 +55,11 @@ __device__ long long g_phase_last_h;
 #endif
 constexpr int TR_STEPS = 8, TR_POINTS = 64;
 __device__ long long g_trace[8][TR_STEPS][TR_POINTS];
+__device__ long long g_looptop[4096];  // clock64 at the loop top of every substep of the traced slice
+#define PF_TR_TOP(r)                                                                              \
+  do {                                                                                            \
+    if ((int)blockIdx.x == PF_TRACE_SLICE && threadIdx.x == 0 && (r) < 4096) g_looptop[(r)] = clock64(); \
+  } while (0)
 #define PF_TR(tr, id)                                                                   \
   do {                                                                                  \
     if ((tr) >= 0 && (threadIdx.x & 31) == 0) g_trace[threadIdx.x >> 5][(tr)][(id)] = clock64(); \
@@ -62,6 +67,9 @@ __device__ long long g_trace[8][TR_STEPS][TR_POINTS];
 #else
 #define PF_TR(tr, id) \
   do {                \
+  } while (0)
+#define PF_TR_TOP(r) \
+  do {               \
   } while (0)
 #endif
 

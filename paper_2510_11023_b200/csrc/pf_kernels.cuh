@@ -379,63 +379,115 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned by
 
 // Helper CTA: the far-history tiles of block (R0, J) with the history rows
 // streamed through shared memory by TMA bulk copies: stages of 8 rows (one
-// 4 KB copy per row into a 64 B-padded slot: bank-conflict-free fragment
-// loads), NS stages in flight on mbarriers, thread 0 the producer.  Warp w
-// computes batch w over the k-steps in ascending order -- the arithmetic and
-// order of tc_far_block, so the tile is bitwise the inline one.
+// 4 KB copy per row into a 64 B-padded slot: minimal-wavefront fragment
+// loads), NS stages on full/empty mbarrier pairs -- no CTA-wide barrier in the
+// row loop.  Warp w consumes batch w of every stage (k-steps in ascending
+// order: the arithmetic and order of tc_far_block, so the tile is bitwise the
+// inline one) and releases the slot with one arrive; thread 0 refills the slot
+// of the stage before the one its warp just finished (that slot's 8 arrivals
+// are almost always in by then), so NS - 1 stages of copies stay in flight.
 struct TmaRing {
   double* buf;                  // NS stages x 8 rows x (size + 8) doubles
-  unsigned long long* full;     // NS mbarriers
+  unsigned long long* full;     // NS mbarriers (1 arrival + the stage's bytes)
+  unsigned long long* empty;    // NS mbarriers (8 arrivals: one per consumer warp)
   int NS;
   long long issued;             // stages issued so far (running: mbarrier phases)
 };
 
-__device__ __forceinline__ void tc_far_block_tma(const double* __restrict__ path, const double* __restrict__ row0,
-                                                 int size, const double* __restrict__ aw,
-                                                 const double* __restrict__ bfine, int R0, int J, double* out,
-                                                 TmaRing& ring) {
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Stream history rows 1 + 8 st .. 8 + 8 st of stages st = st0 .. st1-1 through the ring and
+// accumulate them into TT target tiles at once (tile u: target rows R0[u]+1 .. R0[u]+8):
+// one set of B fragments (the rows) feeds TT DMMAs, so a row is read once per TT tiles.
+// Warp w owns the 64-mode batch w; acc[u][g] is its m8n8 fragment of tile u, group g.
+template <int TT>
+__device__ __forceinline__ void tc_stream(const double* __restrict__ path, int size, const double* __restrict__ aw,
+                                          const int (&R0)[TT], int st0, int st1, double (&acc)[TT][8][2],
+                                          TmaRing& ring) {
   const int NB = size / TC_BATCH, pitch = size + 8;
-  const int nstg = J / 8;  // J = (beta - 1) HB: whole stages of 8 rows
+  const int nstg = st1 - st0;
+  if (nstg <= 0) return;
   const long long g0 = ring.issued;
+  const int NS = ring.NS;
+  // thread 0: copy stage st0 + i into its slot, once the slot's previous use is released
   auto issue = [&](int i) {
-    const int slot = (int)((g0 + i) % ring.NS);
+    const long long g = g0 + i;
+    const int slot = (int)(g % NS);
+    const long long use = g / NS;
+    if (use > 0) mbar_wait(ring.empty + slot, (unsigned)((use - 1) & 1));
     double* dst = ring.buf + (size_t)slot * 8 * pitch;
     mbar_expect_tx(ring.full + slot, 8u * (unsigned)size * 8u);
 #pragma unroll
     for (int t = 0; t < 8; ++t)
-      tma_load(dst + (size_t)t * pitch, path + (size_t)(1 + 8 * i + t) * size, (unsigned)size * 8u, ring.full + slot);
+      tma_load(dst + (size_t)t * pitch, path + (size_t)(1 + 8 * (st0 + i) + t) * size, (unsigned)size * 8u,
+               ring.full + slot);
   };
   if (threadIdx.x == 0) {
     asm volatile("fence.proxy.async;" ::: "memory");  // path rows (generic writes, acquired) -> bulk-copy reads
-    for (int i = 0; i < nstg && i < ring.NS; ++i) issue(i);
+    for (int i = 0; i < nstg && i < NS - 1; ++i) issue(i);
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, k = lane & 3, q = lane >> 2;
-  double acc[8][2];
-#pragma unroll
-  for (int g = 0; g < 8; ++g) acc[g][0] = acc[g][1] = 0.0;
   for (int i = 0; i < nstg; ++i) {
-    const int slot = (int)((g0 + i) % ring.NS);
-    mbar_wait(ring.full + slot, (unsigned)(((g0 + i) / ring.NS) & 1));
+    // keep NS - 1 stages in flight: stage i + NS - 1 goes into the slot stage i - 1 used
+    if (threadIdx.x == 0 && i + NS - 1 < nstg) issue(i + NS - 1);
+    const long long g = g0 + i;
+    const int slot = (int)(g % NS);
+    mbar_wait(ring.full + slot, (unsigned)((g / NS) & 1));
     const double* st = ring.buf + (size_t)slot * 8 * pitch;
     if (w < NB) {
+      double bv[2][8];
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        const int j = 1 + 8 * i + 4 * t + k;
-        const double a = aw[R0 + 1 + q - j];
         const double* bp = st + (size_t)(4 * t + k) * pitch + TC_BATCH * w + q;
-        double bv[8];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) bv[g] = bp[8 * g];
+        for (int g2 = 0; g2 < 8; ++g2) bv[t][g2] = bp[8 * g2];
+      }
 #pragma unroll
-        for (int g = 0; g < 8; ++g) dmma884(acc[g][0], acc[g][1], a, bv[g]);
+      for (int t = 0; t < 2; ++t) {
+        const int j = 1 + 8 * (st0 + i) + 4 * t + k;
+#pragma unroll
+        for (int u = 0; u < TT; ++u) {
+          const double av = aw[R0[u] + 1 + q - j];
+#pragma unroll
+          for (int g2 = 0; g2 < 8; ++g2) dmma884(acc[u][g2][0], acc[u][g2][1], av, bv[t][g2]);
+        }
       }
     }
-    __syncthreads();  // every warp is done with the slot
-    if (threadIdx.x == 0 && i + ring.NS < nstg) issue(i + ring.NS);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(ring.empty + slot);  // this warp is done with the slot
   }
   ring.issued = g0 + nstg;
-  if (w < NB) tc_store_tile(acc, row0, bfine, R0, size, w, out);
 }
+
+// fragment-layout partial tiles in global scratch: [tile][batch w][group g][lane] double2 -- every
+// lane reloads exactly what it stored
+__device__ __forceinline__ void tc_frag_store(double* buf, int tile, int NB, const double (&acc)[8][2]) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* p = reinterpret_cast<double2*>(buf) + ((size_t)(tile * NB + w) * 8) * 32 + lane;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) p[g * 32] = make_double2(acc[g][0], acc[g][1]);
+}
+__device__ __forceinline__ void tc_frag_load(const double* buf, int tile, int NB, double (&acc)[8][2]) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double2* p = reinterpret_cast<const double2*>(buf) + ((size_t)(tile * NB + w) * 8) * 32 + lane;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    const double2 v = p[g * 32];
+    acc[g][0] = v.x;
+    acc[g][1] = v.y;
+  }
+}
+
+// Grouping of the TMA-fed helper: the rows older than G + 1 blocks are accumulated into the G
+// tiles of a super-block of G blocks in ONE pass (a quarter of the one-pass-per-tile traffic:
+// late in a sweep every helper streams its slice's whole path per block, 269 MB per block
+// period at config 3 -- more than HBM delivers); the last (G + t) blocks of rows are appended
+// per tile.  Every accumulator still takes its rows in ascending order: bitwise tc_far_block.
+constexpr int TC_G = 4;
+// rows 1..tc_common_extent(S) are accumulated for all tiles of super-block S together
+__host__ __device__ constexpr int tc_common_extent(int S) { return (TC_G * S - TC_G - 1 > 0 ? TC_G * S - TC_G - 1 : 0) * HB; }
 
 // CTA (256 threads = 8 warps): the far-history tiles of every batch, warp w
 // computing batches w, w + 8, ... over all k-steps in ascending order (the
@@ -474,9 +526,9 @@ __device__ __forceinline__ void tc_out_index(int t, int i, int& slot, int& rr, i
 // pseudo-random 0..8 us, so the release/acquire handshake runs under many
 // interleavings; results must stay bitwise those of the inline far history.
 // (compute-sanitizer is closed on this pool: profiles/r02_compute_sanitizer_closed.txt)
-__device__ __forceinline__ void pf_jitter(int a, int b) {
+__device__ __forceinline__ void pf_jitter(int a, int b, int tid0 = 0) {
 #ifdef PF_JITTER
-  if (threadIdx.x == 0) {
+  if ((int)threadIdx.x == tid0) {
     unsigned h = (unsigned)a * 73856093u ^ (unsigned)b * 19349663u ^ (unsigned)PF_JITTER * 83492791u;
     h ^= h >> 13;
     h *= 0x5bd1e995u;
@@ -486,8 +538,131 @@ __device__ __forceinline__ void pf_jitter(int a, int b) {
 #else
   (void)a;
   (void)b;
+  (void)tid0;
 #endif
 }
+
+// Side work of the Q = 1024 fine sweep (k_fine_sweep, SP::kSide): see the comment at its use.
+struct SideState {
+  double wreg;         // side threads 0..7: guess weight j = s of substep r_side + 2, in flight
+  int poll, poll_need; // side thread 0: the helper's ready counter (load in flight) and the value awaited
+};
+
+  struct SideWork {
+    SideState& d_;
+    double2& hfar;
+    double2& cbrk;
+    const Common& c_;
+    const SweepSync& sync;
+    const double2* ring2;
+    double2* prep;
+    double* wguess;
+    const double* brk_b;
+    double* scr;
+    const double* ext;
+    const int& r_side;
+    int bslice, helpers, hps, tau_until;
+    int need_mul;
+    __device__ __forceinline__ const double* tile(int beta) const {
+      return scr + ((size_t)(beta & 1) * (hps + 1)) * 2 * HB * c_.size;
+    }
+    __device__ __forceinline__ const int* ready() const { return sync.ready + (size_t)bslice * hps; }
+    // a (inverse radix-8 pass 1): publish progress, stage the tabulated guess weights, start the
+    // poll of the far tile that all() of the NEXT substep reads (checked in d, three passes later)
+    __device__ __forceinline__ void a() const {
+      const int s = (int)threadIdx.x - 128, r = r_side;
+      if (helpers && r >= 1 && (r - 1) % HB == 0) {  // rows 0..r-1 are in the path (written before the last barrier)
+        pf_jitter(bslice + 1000003, (r - 1) / HB, 128);
+        if (s == 0) st_release(sync.progress + bslice, r - 1);
+      }
+      if (s < 8) {  // weights of r + 1 (loaded a substep ago) to shared memory; those of r + 2 into flight
+        wguess[s] = d_.wreg;
+        const int r2 = r + 2;
+        d_.wreg = (r2 < tau_until && r2 <= c_.m) ? ext[(size_t)r2 * 8 + s] : 0.0;
+      }
+      if (s == 0) {
+        // substep r + 2 opens block (r + 1) / HB when (r + 1) % HB == 0
+        d_.poll_need = (helpers && (r + 1) % HB == 0 && r + 2 <= c_.m) ? need_mul * ((r + 1) / HB + 1) : 0;
+        if (d_.poll_need) d_.poll = ld_acquire(ready());
+      }
+    }
+    // every thread, after a's barrier: its far-tile and bracket entries of substep r + 1
+    // (the tile was confirmed in d of the substep before, or before the loop)
+    __device__ __forceinline__ void all() const {
+      const int r = r_side;
+      if (r + 1 > c_.m) return;
+      const double* frow = tile(r / HB) + (size_t)(r % HB) * c_.size + threadIdx.x;
+      hfar = make_double2(__ldcg(frow), __ldcg(frow + 256));
+      if (brk_b) {
+        const double* brow = brk_b + (size_t)r * c_.size + threadIdx.x;
+        cbrk = make_double2(__ldcg(brow), __ldcg(brow + 256));
+      }
+    }
+    // near rows q0 <= q < q1 back from row r1 (ring), on top of (a0, a1); guess terms when GUESS
+    template <int Q0, int Q1, bool GUESS>
+    __device__ __forceinline__ void rows(int r1, int J1, int p1, const double* w, int tp, double& a0, double& a1,
+                                         double& g0, double& g1) const {
+      double2 vv[Q1 - Q0];
+#pragma unroll
+      for (int q = Q0; q < Q1; ++q) vv[q - Q0] = ring2[((r1 - q) & (NR - 1)) * 256 + tp];  // (unused rows: never enabled)
+#pragma unroll
+      for (int q = Q0; q < Q1; ++q) {
+        if (r1 - q > J1) {
+          a0 = fma(c_.anear[q], vv[q - Q0].x, a0);
+          a1 = fma(c_.anear[q], vv[q - Q0].y, a1);
+        }
+        if (GUESS && q - 1 <= EXT && q - 1 <= p1) {  // guess weight j = q - 1 takes row r1 - 1 - j
+          g0 = fma(w[q - 1], vv[q - Q0].x, g0);
+          g1 = fma(w[q - 1], vv[q - Q0].y, g1);
+        }
+      }
+    }
+    // b (inverse radix-8 pass 2): near rows r1-2 .. r1-8 and the guess terms of the older rows -> prep
+    __device__ __forceinline__ void b() const {
+      const int s = (int)threadIdx.x - 128, r = r_side, r1 = r + 1;
+      if (r1 > c_.m) return;
+      const int J1 = far_extent(r / HB);
+      const bool tau1 = r1 >= 2 && r1 < tau_until;
+      const int pk = r1 - 1 < EXO ? r1 - 1 : EXO;
+      const int p1 = tau1 ? (r1 - 1 < EXT ? r1 - 1 : EXT) : pk;
+      double w[EXT + 1];
+#pragma unroll
+      for (int j = 1; j <= EXT; ++j) w[j] = tau1 ? wguess[j] : (j <= EXO ? kExtrap[pk][j] : 0.0);
+      w[0] = 0.0;
+      double a[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, g[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      rows<2, 9, true>(r1, J1, p1, w, s, a[0][0], a[0][1], g[0][0], g[0][1]);
+      rows<2, 9, true>(r1, J1, p1, w, s + 128, a[1][0], a[1][1], g[1][0], g[1][1]);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        prep[s + 128 * k] = make_double2(a[k][0], a[k][1]);
+        prep[256 + s + 128 * k] = make_double2(g[k][0], g[k][1]);
+      }
+    }
+    // c (forward radix-8 pass 1): near rows r1-9 .. r1-15 (present from the block's second substep on)
+    __device__ __forceinline__ void c() const {
+      const int s = (int)threadIdx.x - 128, r = r_side, r1 = r + 1;
+      if (r1 > c_.m || r1 - 9 <= far_extent(r / HB)) return;
+      const int J1 = far_extent(r / HB);
+      double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        double2 h = prep[s + 128 * k];
+        rows<9, NR, false>(r1, J1, 0, nullptr, s + 128 * k, h.x, h.y, g0, g1);
+        prep[s + 128 * k] = h;
+      }
+    }
+    // d (forward radix-8 pass 2): the far tile polled in a must be published
+    __device__ __forceinline__ void d() const {
+      if ((int)threadIdx.x == 128 && d_.poll_need) {
+        int ns = 32;
+        while (d_.poll < d_.poll_need) {
+          __nanosleep(ns);
+          ns = ns < 256 ? 2 * ns : ns;
+          d_.poll = ld_acquire(ready());
+        }
+      }
+    }
+};
 
 // Fine sweep.  Grid = nslices slice CTAs (+ nslices helper CTAs when
 // `helpers`, launched cooperatively so all are co-resident).  A helper owns
@@ -525,7 +700,10 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   const bool tc = NT == 256 && c.size % TC_BATCH == 0 && (hps > 1 || c.far_tc > 0);
   // split helpers: each 64-mode batch's k-steps in PK interleaved parts, one (batch, part) unit per helper round
   const int PK = tc_parts(hps, NB);
-  const size_t parts_len = (tc && hps > 1) ? (size_t)2 * NB * PK * 512 : 0;
+  // (one TMA-fed helper: the common partial tiles of two super-blocks, [parity][TC_G][HB][size])
+  // (sized by capability, not by the engine selected: launch_fine's scr_stride)
+  const bool tc_cap = NT == 256 && c.size % TC_BATCH == 0;
+  const size_t parts_len = (tc_cap && hps > 1) ? (size_t)2 * NB * PK * 512 : tc_cap ? (size_t)2 * TC_G * HB * c.size : 0;
   double* scr = c.scratch + (size_t)b * ((size_t)2 * (hps + 1) * 2 * HB * c.size + parts_len);
   auto slot = [&](int parity, int h) { return scr + ((size_t)parity * (hps + 1) + h) * 2 * HB * c.size; };
   double* parts = scr + (size_t)2 * (hps + 1) * 2 * HB * c.size;
@@ -544,17 +722,21 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       used = aw_bytes;
     }
     // the one helper of a slice streams the history rows by TMA (stages behind the weights)
-    TmaRing ring{nullptr, nullptr, 0, 0};
-    if (hps == 1 && c.far_tc == 2 && aw != c.afine) {
+    TmaRing ring{nullptr, nullptr, nullptr, 0, 0};
+    if (hps == 1 && c.far_tc == 2 && aw != c.afine && NB <= NT / 32) {  // (warp w streams batch w)
       const size_t stage = sizeof(double) * 8 * (size_t)(c.size + 8);
       const size_t avail = (size_t)smem_total - used - 128;
       const int NS = (int)min((size_t)6, avail / stage);
       if (NS >= 2) {
         ring.full = reinterpret_cast<unsigned long long*>(smem + used);
+        ring.empty = ring.full + 8;
         ring.buf = reinterpret_cast<double*>(smem + used + 128);
         ring.NS = NS;
         if (threadIdx.x == 0) {
-          for (int i = 0; i < NS; ++i) mbar_init(ring.full + i, 1);
+          for (int i = 0; i < NS; ++i) {
+            mbar_init(ring.full + i, 1);
+            mbar_init(ring.empty + i, 8);
+          }
           asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
       }
@@ -582,11 +764,49 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       double* hs = slot(beta & 1, 0);
       const int R0 = beta * HB;
       const double* row0 = J > 0 ? path : (c.x_start ? c.x_start : U + (size_t)n * c.size);
-      if (hps == 1) {  // the slice's one helper: batch w on warp w
-        if (ring.NS)
-          tc_far_block_tma(path, row0, c.size, aw, c.bfine, R0, J, hs, ring);
-        else
-          tc_far_block(path, row0, c.size, aw, c.bfine, R0, J, hs);
+      if (hps == 1 && ring.NS) {
+        // grouped TMA-fed helper (see TC_G): (a) tile beta = its super-block's common partial + the
+        // rows after it; (b) a quarter of the next super-block's common pass
+        const int S = beta / TC_G, t = beta % TC_G;
+        const int Jc = tc_common_extent(S);
+        {
+          double acc[1][8][2];
+          if (Jc > 0 && w < NB) {
+            tc_frag_load(parts + (size_t)(S & 1) * TC_G * HB * c.size, t, NB, acc[0]);
+          } else {
+#pragma unroll
+            for (int g = 0; g < 8; ++g) acc[0][g][0] = acc[0][g][1] = 0.0;
+          }
+          const int r0s[1] = {R0};
+          tc_stream<1>(path, c.size, aw, r0s, Jc / 8, J / 8, acc, ring);
+          if (w < NB) tc_store_tile(acc[0], row0, c.bfine, R0, c.size, w, hs);
+        }
+        PF_TH(12);
+        cta_publish_add(sync.ready + (size_t)b * hps, NB);
+        const int Jn = tc_common_extent(S + 1);  // <= far_extent(TC_G S) <= J: those rows are in the path
+        if (Jn > 0 && TC_G * (S + 1) < nblocks) {
+          const int nst = Jn / 8, st0 = t * nst / TC_G, st1 = (t + 1) * nst / TC_G;
+          double* pn = parts + (size_t)((S + 1) & 1) * TC_G * HB * c.size;
+          double acc[TC_G][8][2];
+          int r0s[TC_G];
+#pragma unroll
+          for (int u = 0; u < TC_G; ++u) {
+            r0s[u] = (TC_G * (S + 1) + u) * HB;
+            if (t > 0 && w < NB) {
+              tc_frag_load(pn, u, NB, acc[u]);
+            } else {
+#pragma unroll
+              for (int g = 0; g < 8; ++g) acc[u][g][0] = acc[u][g][1] = 0.0;
+            }
+          }
+          tc_stream<TC_G>(path, c.size, aw, r0s, st0, st1, acc, ring);
+          if (w < NB) {
+#pragma unroll
+            for (int u = 0; u < TC_G; ++u) tc_frag_store(pn, u, NB, acc[u]);
+          }
+        }
+      } else if (hps == 1) {  // the slice's one helper: batch w on warp w
+        tc_far_block(path, row0, c.size, aw, c.bfine, R0, J, hs);
         PF_TH(12);
         cta_publish_add(sync.ready + (size_t)b * hps, NB);
       } else {  // split helpers (sequential solver): unit (batch, part) -> helper unit mod hps
@@ -635,7 +855,11 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       aw = s_aw;
     }
     for (int beta = 0; beta < nblocks; ++beta) {
+#ifdef PF_EXP_FARCAP
+      const int J = far_extent(beta) < PF_EXP_FARCAP ? far_extent(beta) : PF_EXP_FARCAP;  // timing experiment: wrong numerics
+#else
       const int J = far_extent(beta);
+#endif
       PF_TH(14);
       if (J > 0) {
         if (threadIdx.x == 0) {
@@ -736,6 +960,8 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     }
   }
   if (EPT == 2 && ring) reinterpret_cast<double2*>(ring)[threadIdx.x] = make_double2(x[0], x[EPT - 1]);
+  // path row 0 is read across threads by the inline tensor-core far history of block 0
+  __syncthreads();
   const double* hs = nullptr;
   int J = 0;
   double hnext[EPT], cnext[EPT];  // this block's far rows, prefetched one substep ahead
@@ -762,6 +988,54 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
   double wnext[EXT + 1];
 #pragma unroll
   for (int j = 0; j <= EXT; ++j) wnext[j] = (2 < tau_until && c.m >= 2) ? ext[(size_t)2 * 8 + j] : 0.0;
+  if constexpr (SP::kSide) {
+  // ---- Q = 1024 engine: warps 4-7 idle in the radix-8 passes prepare substep r + 1 ----
+  // While warps 0-3 run the two inverse radix-8 passes of substep r's setup transform,
+  // warps 4-7 (side threads, two double2 ring columns = four modes each) do everything
+  // of substep r + 1 that does not need x_r: the helper handshake at block boundaries
+  // (publish progress, wait for the far tile: stage a), the near-history rows r - 1,
+  // r - 2, ... and the PCG guess terms of the older rows (stage b, shared memory only).
+  // Between the stages every thread prefetches its far-tile and bracket entries of
+  // substep r + 1 (a whole substep ahead of their use).  The owner thread then finishes
+  // with h = a_1 x_r + (far + h'), guess = w_0 x_r + g'.
+  // (The ring always fits at this size: launch_fine checks it.)
+  const double2* ring2 = reinterpret_cast<const double2*>(ring);
+  double2* prep = reinterpret_cast<double2*>(smem + ring_off + sizeof(double) * NR * 2 * NT);  // [h' | g'][NT]
+  __shared__ double s_wguess[8];  // tabulated guess weights of the substep being prepared
+  const int tid = threadIdx.x;
+  SideState sd;
+  sd.wreg = 0.0;  // (substep 1 has no tabulated weights: its guess is x_0)
+  sd.poll = sd.poll_need = 0;
+  int r_side = 0;  // the substep the side stages run beside (they prepare r_side + 1)
+  double2 hfar = make_double2(0.0, 0.0), cbrk = make_double2(0.0, 0.0);
+  SideWork side{sd,      hfar, cbrk,    c,       sync,      ring2,     prep, s_wguess, brk_b, scr, ext, r_side,
+         b,       helpers, hps,  tau_until, tc ? NB : 1};
+  // far tile of block `bt`, computed inline when there is no helper
+  auto inline_tile = [&](int bt) {
+    double* s0 = slot(bt & 1, 0);
+    if (tc)
+      tc_far_block(path, path, c.size, c.afine, c.bfine, bt * HB, far_extent(bt), s0);
+    else
+      far_history_block<NT, EPT, JT>(c, path, c.afine, bt * HB, far_extent(bt), s0);
+  };
+  if (!helpers) {
+    inline_tile(0);
+  } else if (tid == 0) {  // tile 0 (b_r x_0 rows: the helper needs no progress for it)
+    int ns = 32;
+    while (ld_acquire(side.ready()) < (tc ? NB : 1)) {
+      __nanosleep(ns);
+      ns = ns < 256 ? 2 * ns : ns;
+    }
+  }
+  __syncthreads();
+  if (tid >= 128) side.a();  // r_side = 0: prepares substep 1 (no near rows, guess x_0)
+  side.all();
+  if (tid >= 128) {
+    side.b();
+    side.d();
+  }
+  __syncthreads();
+  double w0next = 1.0;  // guess weight of x_{r-1} at substep r (r = 1: the guess is x_0)
   for (int r = 1; r <= c.m; ++r) {
     const double t = (double)n * c.dT + (double)(r - 1) * c.dt;
     const int rr = (r - 1) % HB;
@@ -770,6 +1044,66 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     sp.tr = ((int)blockIdx.x == PF_TRACE_SLICE && r >= PF_TRACE_R0 && r < PF_TRACE_R0 + TR_STEPS) ? r - PF_TRACE_R0 : -1;
 #endif
     PF_TR(sp.tr, 0);
+    PF_TR_TOP(r);
+    PF_T(10);
+    if (c.cancel && rr == 0 && beta > 0 &&
+        __syncthreads_or(threadIdx.x == 0 && *(volatile const int*)c.cancel != 0)) {
+      st.code = ST_CANCEL;  // speculative sweep after convergence: discarded
+      st.r = r;
+      break;
+    }
+    // no helper: the tile of the block that opens at r + 1 (its rows end a block ago), before stage a needs it
+    if (!helpers && r % HB == 0 && r < c.m) {
+      inline_tile(r / HB);
+      __syncthreads();
+    }
+    PF_TR(sp.tr, 1);
+    PF_T(8);
+    const double2 hp = prep[tid], gp = prep[256 + tid];
+    const double w0 = w0next;
+    {
+      const int r1 = r + 1;
+      const bool ut = r1 < tau_until && r1 <= c.m;
+      const int pk = r1 - 1 < EXO ? r1 - 1 : EXO;
+      w0next = ut ? ext[(size_t)r1 * 8] : kExtrap[pk][0];
+    }
+    double h[EPT], ct[EPT], xg[EPT], xn[EPT];
+    h[0] = hfar.x + hp.x;
+    h[1] = hfar.y + hp.y;
+    if (r >= 2) {
+      h[0] = fma(c.anear[1], x[0], h[0]);
+      h[1] = fma(c.anear[1], x[1], h[1]);
+    }
+    xg[0] = fma(w0, x[0], gp.x);
+    xg[1] = fma(w0, x[1], gp.y);
+    ct[0] = cbrk.x;
+    ct[1] = cbrk.y;
+    r_side = r;
+    PF_TR(sp.tr, 2);
+    PF_T(9);
+    const int code = sp.step(c.fn, x, xg, t, c.gam_f, h, ct, xn, st, side);
+    if (code != ST_OK) {
+      st.code = code;
+      st.r = r;
+      break;
+    }
+    x[0] = xn[0];
+    x[1] = xn[1];
+    path[(size_t)r * c.size + tid] = x[0];
+    path[(size_t)r * c.size + tid + NT] = x[1];
+    reinterpret_cast<double2*>(ring)[(r & (NR - 1)) * NT + tid] = make_double2(x[0], x[1]);
+    PF_TR(sp.tr, 47);
+  }
+  } else {
+  for (int r = 1; r <= c.m; ++r) {
+    const double t = (double)n * c.dT + (double)(r - 1) * c.dt;
+    const int rr = (r - 1) % HB;
+    const int beta = (r - 1) / HB;
+#ifdef PF_TRACE
+    sp.tr = ((int)blockIdx.x == PF_TRACE_SLICE && r >= PF_TRACE_R0 && r < PF_TRACE_R0 + TR_STEPS) ? r - PF_TRACE_R0 : -1;
+#endif
+    PF_TR(sp.tr, 0);
+    PF_TR_TOP(r);
     PF_T(10);
     if (c.cancel && rr == 0 && beta > 0 &&
         __syncthreads_or(threadIdx.x == 0 && *(volatile const int*)c.cancel != 0)) {
@@ -942,6 +1276,7 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
       reinterpret_cast<double2*>(ring)[(r & (NR - 1)) * NT + threadIdx.x] = make_double2(x[0], x[EPT - 1]);
     PF_TR(sp.tr, 47);
   }
+  }  // !SP::kSide
   if (st.code == ST_OK) {
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {

@@ -339,13 +339,29 @@ __device__ __forceinline__ void first_fwd10(cd (&x)[4], cd* __restrict__ b) {
   b[sw10(4 * j + 3)] = x[3];
 }
 
+// Side work: the radix-8 passes keep only warps 0-3 busy (128 butterflies), so the
+// caller can hand warps 4-7 independent work -- a() and b() run beside the inverse
+// transform's two radix-8 passes, c() and d() beside the forward transform's
+// (k_fine_sweep: the next substep's near history, PCG guess and helper handshake, off
+// the substep's critical path); all() runs on every thread after a()'s barrier.
+struct NoSide {
+  __device__ __forceinline__ void a() const {}
+  __device__ __forceinline__ void all() const {}  // every thread, after the first pass's barrier
+  __device__ __forceinline__ void b() const {}
+  __device__ __forceinline__ void c() const {}    // beside the forward transform's two radix-8 passes
+  __device__ __forceinline__ void d() const {}
+};
+
 // (tr, id0: PF_TRACE timeline slot of the first pass; no code in the product build)
-template <int NT>
-__device__ __forceinline__ cd* inv_passes10(cd* A, cd* B, const cd* tw, int tr = -1, int id0 = 0) {
+template <int NT, class Side = NoSide>
+__device__ __forceinline__ cd* inv_passes10(cd* A, cd* B, const cd* tw, int tr, int id0, Side& side) {
   r8_pass10<true, 1, 0>(A, B, tw);
+  if (threadIdx.x >= 128) side.a();
   bar<NT>();
+  side.all();
   PF_TR(tr, id0);
   r8_pass10<true, 8, T10_R8_8>(B, A, tw);
+  if (threadIdx.x >= 128) side.b();
   bar<NT>();
   PF_TR(tr, id0 + 1);
   r4_pass10<true, 64, T10_R4_64>(A, B, tw);
@@ -354,15 +370,17 @@ __device__ __forceinline__ cd* inv_passes10(cd* A, cd* B, const cd* tw, int tr =
   return B;
 }
 
-template <int NT>
-__device__ __forceinline__ cd* fwd_passes10(cd* Y, cd* X, const cd* tw, int tr = -1, int id0 = 0) {
+template <int NT, class Side = NoSide>
+__device__ __forceinline__ cd* fwd_passes10(cd* Y, cd* X, const cd* tw, int tr, int id0, Side& side) {
   r4_pass10<false, 4, T10_R4_4>(Y, X, tw);
   bar<NT>();
   PF_TR(tr, id0);
   r8_pass10<false, 16, T10_R8_16>(X, Y, tw);
+  if (threadIdx.x >= 128) side.c();
   bar<NT>();
   PF_TR(tr, id0 + 1);
   r8_pass10<false, 128, T10_R8_128>(Y, X, tw);
+  if (threadIdx.x >= 128) side.d();
   bar<NT>();
   PF_TR(tr, id0 + 2);
   return X;
@@ -387,6 +405,12 @@ struct Sine1D {
   // phase factors of the owned modes, ph[k] and ph[Q-k], kept in registers (every
   // synthesis input and analysis gather of every substep reads them)
   static constexpr bool kPhReg = EPT <= 2;  // (EPT = 4 would spill)
+  // the Q = 1024 engine leaves warps 4-7 idle in its radix-8 passes: k_fine_sweep gives them side work
+#ifdef PF_NO_SIDE  // A/B builds (tools/): the owner threads do the near history at the loop top
+  static constexpr bool kSide = false;
+#else
+  static constexpr bool kSide = (LG == 10 && NT == 256 && EPT == 2);
+#endif
   cd phk[EPT], phq[EPT];
   int tr = -1;  // PF_TRACE timeline row of the current substep (-1: not traced)
 
@@ -486,7 +510,8 @@ struct Sine1D {
     PF_TR(tr, id0);
     cd* Z;
     if constexpr (LG == 10 && NT == 256) {
-      cd* X = inv_passes10<NT>(A, B, twp, tr, id0 + 1);
+      NoSide ns;
+      cd* X = inv_passes10<NT>(A, B, twp, tr, id0 + 1, ns);
       cd* Y = (X == A) ? B : A;
       cd v[4];
       last_inv10(X, twp, v);
@@ -495,7 +520,7 @@ struct Sine1D {
       first_fwd10(v, Y);
       bar<NT>();
       PF_TR(tr, id0 + 4);
-      Z = fwd_passes10<NT>(Y, X, twp, tr, id0 + 5);
+      Z = fwd_passes10<NT>(Y, X, twp, tr, id0 + 5, ns);
     } else if constexpr (kFuse) {
       constexpr int P = LG / 2;
       cd* X = fft_passes<LG, NT, true, 0, P - 1>(A, B, twp);
@@ -593,8 +618,16 @@ struct Sine1D {
 
   // xguess: PCG initial guess (the caller extrapolates from the path; it
   // only changes the iteration count, not the solution beyond pcg_tol).
+  __device__ __forceinline__ int step(const Fn& fn, const double* xprev, const double* xguess, double t, double gam,
+                                      const double* hist, const double* contrib, double* xout, Status& st) {
+    NoSide ns;
+    return step(fn, xprev, xguess, t, gam, hist, contrib, xout, st, ns);
+  }
+
+  // side: work for warps 4-7 beside the setup transform's radix-8 passes (Q = 1024 only; see NoSide)
+  template <class Side>
   __device__ int step(const Fn& fn, const double* xprev, const double* xguess, double t, double gam,
-                      const double* hist, const double* contrib, double* xout, Status& st) {
+                      const double* hist, const double* contrib, double* xout, Status& st, Side& side) {
     PF_T(0);
     // --- synthesis pair: u = S c_prev, v0 = S' x0 ------------------------
     {
@@ -624,7 +657,7 @@ struct Sine1D {
     // one block reduction fewer per substep (the FFT itself does not depend
     // on them; a non-finite D is reported before any solve)
     if constexpr (LG == 10 && NT == 256) {
-      cd* X = inv_passes10<NT>(A, B, twp, tr, 4);
+      cd* X = inv_passes10<NT>(A, B, twp, tr, 4, side);
       cd* Y = (X == A) ? B : A;
       PF_T(1);
       cd v[4];
@@ -640,7 +673,7 @@ struct Sine1D {
       bar<NT>();
       PF_TR(tr, 7);
       PF_T(2);
-      Z = fwd_passes10<NT>(Y, X, twp, tr, 8);
+      Z = fwd_passes10<NT>(Y, X, twp, tr, 8, side);
     } else if constexpr (kFuse) {
       constexpr int P = LG / 2;
       cd* X = fft_passes<LG, NT, true, 0, P - 1>(A, B, twp);

@@ -75,9 +75,10 @@ def test_handshake_bitwise_under_jitter():
 
 @pytest.mark.parametrize("far_tc", ["1", "2"])
 def test_tensor_core_far_history_helper_bitwise_inline(far_tc):
-    """PF_FAR_TC=1 (DMMA, direct loads) / 2 (DMMA fed by TMA bulk copies): the
+    """PF_FAR_TC=1 (DMMA, direct loads) / 2 (DMMA fed by TMA bulk copies, the old
+    rows accumulated for four tiles per pass: the default at M = 512): the
     helper CTA's far history under jitter == the slice CTA's inline DMMA path,
-    bitwise, and the DFMA default to rounding."""
+    bitwise, and the DFMA engine (PF_FAR_TC=0) to rounding."""
     import torch
 
     if not torch.cuda.is_available():
@@ -86,5 +87,14 @@ def test_tensor_core_far_history_helper_bitwise_inline(far_tc):
     inline = _run({"PF_NO_HELPERS": "1", "PF_FAR_TC": "1"})
     assert int(helper["helpers"]) >= 1 and int(inline["helpers"]) == 0
     np.testing.assert_array_equal(helper["sweep"], inline["sweep"])
-    dfma = _run({})
+    dfma = _run({"PF_FAR_TC": "0"})
     assert np.linalg.norm(helper["sweep"] - dfma["sweep"]) <= 1e-13 * np.linalg.norm(dfma["sweep"])
+    if far_tc == "2":
+        # engine 2 is the default at M = 512 (grouped passes over the old rows, TC_G tiles per pass)
+        assert np.array_equal(_run({})["sweep"], helper["sweep"])
+        # the DFMA register-tile helper (PF_FAR_TC=0) under jitter == its inline path, bitwise
+        dfma_jit = _run({"PARAFRAC_B200_LIB": JITTER, "PF_FAR_TC": "0"})
+        dfma_inline = _run({"PF_NO_HELPERS": "1", "PF_FAR_TC": "0"})
+        assert int(dfma_jit["helpers"]) >= 1 and int(dfma_inline["helpers"]) == 0
+        np.testing.assert_array_equal(dfma_jit["sweep"], dfma_inline["sweep"])
+        np.testing.assert_array_equal(dfma["sweep"], dfma_inline["sweep"])

@@ -42,3 +42,17 @@ nxt = [t[:, s + 1, 0].min() - t0[s] for s in steps if s + 1 in steps]
 print("substep length (loop top to loop top):", np.mean(nxt) if nxt else None)
 for s in steps:
     print("substep", s, "block-start" if (s % 8) == ((513 - 1) % 8) else "", "length", (t[:, s + 1, 0].min() - t0[s]) if s + 1 in steps else None)
+
+# substep durations over the whole sweep (loop top to loop top), in windows of 64 substeps
+m = c["m"]
+lt = (C.c_longlong * (m + 1))()
+_lib.lib.pf_debug_looptop(lt, m + 1)
+lt = np.array(lt[:], dtype=np.int64)
+d = np.diff(lt[1:m + 1]).astype(float)
+print("substep duration by window of 64 substeps (mean cycles; block-start substeps' mean; max):")
+for w0 in range(0, m - 1, 64):
+    seg = d[w0:w0 + 64]
+    idx = np.arange(w0 + 1, w0 + 1 + len(seg))
+    bs = seg[(idx - 1) % 8 == 0]
+    print(f"  r {w0 + 1:5d}..{w0 + len(seg):5d}: mean {seg.mean():8.0f}  block-start mean {bs.mean() if len(bs) else 0:8.0f}  max {seg.max():8.0f}")
+print("total cycles", lt[m] - lt[1], "=", (lt[m] - lt[1]) / 1.965e6, "ms at 1965 MHz")
