@@ -553,11 +553,21 @@ def _gpu_arm(args, rank, world, local):
 
     parareal = None
     if not args.no_parareal and not dist.is_initialized():
-        t0 = time.perf_counter()
-        it, rep = pfb.parareal_solve(prob, op, grids, tol=cfg["tol"], k_max=P + 1)
-        parareal = {"time_to_tol_s": time.perf_counter() - t0, "iterations": rep.iterations,
+        # one untimed solve (the driver's buffers and streams are allocated on first use), then
+        # the minimum of three timed solves (the reference harness's convention, harness.py:65-73);
+        # the 2-D configs run for seconds: one timed solve
+        reps = 3 if dims == 1 else 1
+        times = []
+        for rep_i in range(reps + (1 if dims == 1 else 0)):
+            t0 = time.perf_counter()
+            it, rep = pfb.parareal_solve(prob, op, grids, tol=cfg["tol"], k_max=P + 1)
+            times.append(time.perf_counter() - t0)
+        timed = times[1:] if dims == 1 else times
+        parareal = {"time_to_tol_s": min(timed), "iterations": rep.iterations,
                     "stop_reason": rep.stop_reason, "final_diff": rep.diffs[-1], "slices": P,
-                    "note": "public API parareal_solve, initial coarse sweep + all iterations"}
+                    "first_call_s": times[0], "timed_solves_s": timed,
+                    "note": "public API parareal_solve, initial coarse sweep + all iterations; "
+                            + ("min of 3 after one untimed solve" if dims == 1 else "one solve")}
     elif not args.no_parareal:
         # multi-GPU time-to-tol: slices sharded over the ranks, one NCCL all-gather
         # of the fine endpoints per iteration, replicated correction (parallel.py)

@@ -221,22 +221,33 @@ struct Reducer {
     buf = 0;
   }
   __device__ __forceinline__ double2 sum2(double a, double b) {
-    // xor butterfly: every lane ends with the bitwise-same sum (IEEE add commutes)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      b += __shfl_xor_sync(0xffffffffu, b, o);
-    }
     if (NT == 32) {
+      // xor butterfly: every lane ends with the bitwise-same sum (IEEE add commutes)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+      }
       __syncwarp();  // orders the warp's smem traffic like the block barrier does
       return make_double2(a, b);
     }
+    // Split butterfly (the same xor-16, 8, 4, 2, 1 tree per value, so the sums are bitwise the
+    // full butterfly's): in the first round the lower half-warp keeps summing a and hands its b
+    // over, the upper half the other way round -- one 64-bit shuffle per round instead of two;
+    // lane 0 ends with the warp's a, lane 16 with its b.
+    const int lane = threadIdx.x & 31;
+    {
+      const bool up = (lane & 16) != 0;
+      const double send = up ? a : b;
+      double keep = up ? b : a;
+      keep += __shfl_xor_sync(0xffffffffu, send, 16);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, o);
+      a = keep;
+    }
     const int w = threadIdx.x >> 5;
     double* slot = red + buf * 128;
-    if ((threadIdx.x & 31) == 0) {
-      slot[4 * w] = a;
-      slot[4 * w + 1] = b;
-    }
+    if ((lane & 15) == 0) slot[4 * w + (lane >> 4)] = a;
     __syncthreads();
     // pairwise (fixed-shape) tree over the warps' partials: log2(NT/32) dependent adds
     double2 v[NT / 32];
@@ -282,25 +293,38 @@ struct Reducer {
     return make_double3(sa, sb, sc);
   }
   __device__ __forceinline__ double4 sum4(double a, double b, double c, double d) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      b += __shfl_xor_sync(0xffffffffu, b, o);
-      c += __shfl_xor_sync(0xffffffffu, c, o);
-      d += __shfl_xor_sync(0xffffffffu, d, o);
-    }
     if (NT == 32) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+      }
       __syncwarp();
       return make_double4(a, b, c, d);
     }
+    // split butterfly (see sum2): round xor-16 halves the four values to two per lane, round
+    // xor-8 to one; lanes 0, 8, 16, 24 end with the warp's a, b, c, d -- 6 shuffles, not 20
+    const int lane = threadIdx.x & 31;
+    {
+      const bool up16 = (lane & 16) != 0, up8 = (lane & 8) != 0;
+      // lower half keeps (a, b), upper half keeps (c, d)
+      double k0 = up16 ? c : a, k1 = up16 ? d : b;
+      const double s0 = up16 ? a : c, s1 = up16 ? b : d;
+      k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+      k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+      // within a half: lanes with bit 3 clear keep k0, the others k1
+      double keep = up8 ? k1 : k0;
+      const double send = up8 ? k0 : k1;
+      keep += __shfl_xor_sync(0xffffffffu, send, 8);
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, o);
+      a = keep;  // lane 0: a, lane 8: b, lane 16: c, lane 24: d
+    }
     const int w = threadIdx.x >> 5;
     double* slot = red + buf * 128;
-    if ((threadIdx.x & 31) == 0) {
-      slot[4 * w] = a;
-      slot[4 * w + 1] = b;
-      slot[4 * w + 2] = c;
-      slot[4 * w + 3] = d;
-    }
+    if ((lane & 7) == 0) slot[4 * w + (lane >> 3)] = a;
     __syncthreads();
     double2 v[NT / 32], u[NT / 32];
 #pragma unroll

@@ -598,22 +598,25 @@ struct SideState {
         cbrk = make_double2(__ldcg(brow), __ldcg(brow + 256));
       }
     }
-    // near rows q0 <= q < q1 back from row r1 (ring), on top of (a0, a1); guess terms when GUESS
+    // near rows Q0 <= q < Q1 back from row r1 (ring), on top of (a0, a1); guess terms when GUESS.
+    // The row masks are warp-uniform, so they select the WEIGHT (0 for a row outside the
+    // range) instead of the result: fma(0, v, a) == a for the finite rows the ring holds
+    // (the kernel zero-fills it), and no per-element selects are left in the chains.
     template <int Q0, int Q1, bool GUESS>
     __device__ __forceinline__ void rows(int r1, int J1, int p1, const double* w, int tp, double& a0, double& a1,
                                          double& g0, double& g1) const {
       double2 vv[Q1 - Q0];
 #pragma unroll
-      for (int q = Q0; q < Q1; ++q) vv[q - Q0] = ring2[((r1 - q) & (NR - 1)) * 256 + tp];  // (unused rows: never enabled)
+      for (int q = Q0; q < Q1; ++q) vv[q - Q0] = ring2[((r1 - q) & (NR - 1)) * 256 + tp];
 #pragma unroll
       for (int q = Q0; q < Q1; ++q) {
-        if (r1 - q > J1) {
-          a0 = fma(c_.anear[q], vv[q - Q0].x, a0);
-          a1 = fma(c_.anear[q], vv[q - Q0].y, a1);
-        }
-        if (GUESS && q - 1 <= EXT && q - 1 <= p1) {  // guess weight j = q - 1 takes row r1 - 1 - j
-          g0 = fma(w[q - 1], vv[q - Q0].x, g0);
-          g1 = fma(w[q - 1], vv[q - Q0].y, g1);
+        const double wa = (r1 - q > J1) ? c_.anear[q] : 0.0;
+        a0 = fma(wa, vv[q - Q0].x, a0);
+        a1 = fma(wa, vv[q - Q0].y, a1);
+        if (GUESS && q - 1 <= EXT) {  // guess weight j = q - 1 takes row r1 - 1 - j
+          const double wg = (q - 1 <= p1) ? w[q - 1] : 0.0;
+          g0 = fma(wg, vv[q - Q0].x, g0);
+          g1 = fma(wg, vv[q - Q0].y, g1);
         }
       }
     }
@@ -644,12 +647,11 @@ struct SideState {
       if (r1 > c_.m || r1 - 9 <= far_extent(r / HB)) return;
       const int J1 = far_extent(r / HB);
       double g0 = 0.0, g1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        double2 h = prep[s + 128 * k];
-        rows<9, NR, false>(r1, J1, 0, nullptr, s + 128 * k, h.x, h.y, g0, g1);
-        prep[s + 128 * k] = h;
-      }
+      double2 h0 = prep[s], h1 = prep[s + 128];
+      rows<9, NR, false>(r1, J1, 0, nullptr, s, h0.x, h0.y, g0, g1);
+      rows<9, NR, false>(r1, J1, 0, nullptr, s + 128, h1.x, h1.y, g0, g1);
+      prep[s] = h0;
+      prep[s + 128] = h1;
     }
     // d (forward radix-8 pass 2): the far tile polled in a must be published
     __device__ __forceinline__ void d() const {
@@ -1018,6 +1020,8 @@ __global__ void __launch_bounds__(NT) k_fine_sweep(Common c, SPP spp, const doub
     else
       far_history_block<NT, EPT, JT>(c, path, c.afine, bt * HB, far_extent(bt), s0);
   };
+  // ring rows 1..NR-1 hold zeros until their states arrive (masked rows are multiplied by a zero weight)
+  for (int q = 1; q < NR; ++q) reinterpret_cast<double2*>(ring)[q * NT + tid] = make_double2(0.0, 0.0);
   if (!helpers) {
     inline_tile(0);
   } else if (tid == 0) {  // tile 0 (b_r x_0 rows: the helper needs no progress for it)

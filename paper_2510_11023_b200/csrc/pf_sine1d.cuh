@@ -776,14 +776,16 @@ struct Sine1D {
         const int tb = it <= 2 ? 14 + (it - 1) * 16 : 62;
         apply_k(p, kp, tb);
         PF_T(5);
-        double pql = 0.0;
+        double pql = 0.0, rql = 0.0, qql = 0.0;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
           qv[i] = p[i] + gam * kp[i];
           pql = fma(p[i], qv[i], pql);
+          rql = fma(r[i], qv[i], rql);
+          qql = fma(qv[i], qv[i], qql);
         }
         PF_TR(it <= 2 ? tr : -1, tb + 8);
-        const double2 pr = red.sum2(pql, it == 1 ? rzl : 0.0);
+        const double4 pr = red.sum4(pql, it == 1 ? rzl : 0.0, rql, qql);
         PF_TR(it <= 2 ? tr : -1, tb + 9);
         const double pq = pr.x;
         if (it == 1) rz = pr.y;
@@ -792,6 +794,27 @@ struct Sine1D {
         // a zero or non-finite (p, A p) gives a non-finite alpha either way
         const double alpha = rz * rcp_fast(pq);
         if (!isfinite(alpha)) return ST_SOLVER;
+        // |r - alpha q|^2 = (r,r) - 2 alpha (r,q) + alpha^2 (q,q) from the same reduction: when the
+        // residual is already small (cancellation error ~1e-15 (r,r) <= thr / 20) and the
+        // prediction is below thr / 2, the updated residual passes the test below too -- take
+        // x and skip the residual update and its reduction (the common one-iteration solve).
+        // Otherwise the iteration continues exactly as before, so iteration counts and x are
+        // those of the two-reduction loop.
+        {
+          const double pred = fma(alpha, fma(alpha, pr.w, -2.0 * pr.z), rrv);
+#ifdef PF_EXP_PRINT
+          if (threadIdx.x == 0 && blockIdx.x == 1 && (st.solves % 97) == 0)
+            printf("solve %d it %d rr0/bb %.3e thr/bb %.3e pred/bb %.3e\n", st.solves, it, rrv / s0.z, thr / s0.z, pred / s0.z);
+#endif
+#ifndef PF_SINGLE_RED
+#define PF_SINGLE_RED 1
+#endif
+          if (PF_SINGLE_RED && rrv <= 1e13 * thr && pred <= 0.5 * thr) {
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) x[i] = fma(alpha, p[i], x[i]);
+            break;
+          }
+        }
         double rrl = 0.0, rzn = 0.0;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {

@@ -56,3 +56,10 @@ for w0 in range(0, m - 1, 64):
     bs = seg[(idx - 1) % 8 == 0]
     print(f"  r {w0 + 1:5d}..{w0 + len(seg):5d}: mean {seg.mean():8.0f}  block-start mean {bs.mean() if len(bs) else 0:8.0f}  max {seg.max():8.0f}")
 print("total cycles", lt[m] - lt[1], "=", (lt[m] - lt[1]) / 1.965e6, "ms at 1965 MHz")
+# per-warp arrival (cycles since loop top, mean over the traced substeps) at the setup transform's points
+print("per-warp arrival times (warp 0..7):")
+for p in (3, 4, 5, 6, 7, 8, 9, 10, 14, 15, 16):
+    ok = [s for s in steps if (t[:, s, p] > 0).all()]
+    if ok:
+        rel = np.array([[t[w, s, p] - t0[s] for w in range(8)] for s in ok], dtype=float).mean(axis=0)
+        print(f"  {names.get(p, p):40s} " + " ".join(f"{v:6.0f}" for v in rel))
