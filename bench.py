@@ -144,9 +144,22 @@ def sweep_flops_2d(M, m, slices, n_lo, pcg_iterations):
     return f
 
 
-def history_bytes(M, m, slices, hb=8):
-    """HBM bytes of the blocked history: each path row read once per block + written once."""
-    rows_read = sum(((r0 + 1)) for r0 in range(0, m, hb))
+def history_bytes(M, m, slices, hb=8, group=1):
+    """Bytes of the blocked history: each path row read once per block + written once.
+    group = G > 1 (the TMA-fed DMMA helper, pf_kernels.cuh TC_G): the rows older than G + 1
+    blocks are read once per super-block of G blocks, the (G + t) hb newest rows once per tile."""
+    if group <= 1:
+        rows_read = sum(((r0 + 1)) for r0 in range(0, m, hb))
+    else:
+        nblocks = (m + hb - 1) // hb
+        rows_read = 0
+        for beta in range(nblocks):
+            S, t = divmod(beta, group)
+            far = max(beta - 1, 0) * hb
+            common = max(group * S - group - 1, 0) * hb
+            rows_read += far - common                       # appended per tile
+            if t == 0 and group * (S + 1) < nblocks:
+                rows_read += max(group * S - 1, 0) * hb     # next super-block's common pass
     return slices * 8.0 * M * (rows_read + (m + 1) + m * (hb // 2) / hb)
 
 
@@ -509,20 +522,23 @@ def _gpu_arm(args, rank, world, local):
     flops = (sweep_flops(M, m, hi - lo, lo, st["pcg_iterations"], st["solves"]) if dims == 1
              else sweep_flops_2d(M, m, hi - lo, lo, st["pcg_iterations"]))
     achieved_tf = flops / (ms / 1e3) / 1e12
+    # far-history engine of this size: the grouped TMA-fed DMMA helper at M = 512 (1-D), unless overridden
+    hist_group = 4 if (dims == 1 and M == 512 and os.environ.get("PF_FAR_TC", "2") == "2") else 1
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs", 6547.5)
     roof = {"bound": "fp64", "achieved": achieved_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": achieved_tf / FP64_PEAK_TFLOPS, "traffic": None,
-            "bound_note": "FP64 pipe (DFMA; DMMA measured at the same rate on this pool): FP64 has no tcgen05 "
-                          "kind, so the binding compute roof is the FP64 peak, not the bf16 tensor figure",
+            "bound_note": "FP64 pipe (DFMA in the slice CTAs, DMMA.8x8x4 in the helper CTAs; both measured at the "
+                          "same rate on this pool): FP64 has no tcgen05 kind, so the binding compute roof is the "
+                          "FP64 peak, not the bf16 tensor figure",
             "peak_source": "measured FP64 DMMA/DFMA peak (profiles/fp64_peaks_r01.txt); "
                            "MEASURED_PEAKS.json has HBM and bf16 only",
             "flops_per_launch": flops, "pcg_iterations_per_launch": st["pcg_iterations"],
             "solves_per_launch": st["solves"],
             "pcg_iterations_per_solve": st["pcg_iterations"] / max(st["solves"], 1),
-            "hbm_bytes_per_launch_model": history_bytes(M ** dims, m, hi - lo),
+            "hbm_bytes_per_launch_model": history_bytes(M ** dims, m, hi - lo, group=hist_group),
             "hbm_peak_gbs": hbm_peak,
-            "hbm_frac_model": history_bytes(M ** dims, m, hi - lo) / (ms / 1e3) / 1e9 / hbm_peak}
+            "hbm_frac_model": history_bytes(M ** dims, m, hi - lo, group=hist_group) / (ms / 1e3) / 1e9 / hbm_peak}
     try:
         with open(os.path.join(ROOT, "profiles", f"dram_config{args.config}.json")) as f:
             dram = json.load(f)

@@ -32,7 +32,7 @@ namespace {
 
 // Sine variants by log2(Q): (threads per CTA, modes per thread)
 //   LG 2-6: (32, 1)  LG 7: (32, 2)  LG 8: (64, 2)  LG 9: (128, 2)  LG 10: (256, 2)  LG 11: (256, 4)
-enum Variant { V_NONE = 0, V_S2, V_S3, V_S4, V_S5, V_S6, V_S7, V_S8, V_S9, V_S10, V_S11, V_CHEB_128_1 };
+enum Variant { V_NONE = 0, V_S2, V_S3, V_S4, V_S5, V_S6, V_S7, V_S8, V_S9, V_S10, V_S11, V_CHEB_128_1, V_CHEB_512_1 };
 
 struct DevBuf {
   double* p = nullptr;
@@ -102,6 +102,8 @@ struct pf_ctx {
   // pipelined parareal driver (1-D): second F_old buffer, per-parity sweep status,
   // correction chunk state, cancel word, chunk streams and events
   DevBuf fold2;
+  DevBuf cheb_aug;         // global-residence Chebyshev bridge: one augmented system per slice slot (Cheb1D<512, 1>)
+  DevBuf cheb_aug_coarse;  // ... and the coarse kernel's own (it overlaps fine sweeps in the pipelined driver)
   Status* d_status2 = nullptr;
   Status* d_corr_status = nullptr;
   int* d_corr_state = nullptr;  // [parity][4]: same, first changed, failed
@@ -187,7 +189,25 @@ pf::Cheb1DParams cheb_params(const pf_ctx* c) {
   p.nodes = c->d_nodes;
   p.d1 = c->d_d1;
   p.qw = c->d_qw;
+  p.aug_g = c->variant == V_CHEB_512_1 ? c->cheb_aug.p : nullptr;  // (sized by ensure_cheb_aug before every launch)
+  p.aug_stride = (size_t)c->ni * pf::Cheb1D<512, 1>::ld_of(c->ni);
   return p;
+}
+
+// the global-residence Chebyshev systems of a launch start at buffer slot q0 (one slab per CTA)
+inline void offset_slab(pf::Sine1DParams&, size_t) {}
+inline void offset_slab(pf::Cheb1DParams& p, size_t q0) {
+  if (p.aug_g) p.aug_g += q0 * p.aug_stride;
+}
+// the coarse kernel (one CTA) uses its own system slab
+inline void coarse_slab(pf::Sine1DParams&, const pf_ctx*) {}
+inline void coarse_slab(pf::Cheb1DParams& p, const pf_ctx* c) {
+  if (c->variant == V_CHEB_512_1) p.aug_g = c->cheb_aug_coarse.p;
+}
+int ensure_cheb_aug(pf_ctx* c, size_t slots) {
+  if (c->variant != V_CHEB_512_1) return 0;
+  const size_t stride = (size_t)c->ni * pf::Cheb1D<512, 1>::ld_of(c->ni);
+  return c->cheb_aug.ensure(slots * stride);
 }
 
 // Dispatch: binds SP (space type), SPP (its params), NT, EPT and `spp`.
@@ -225,6 +245,8 @@ pf::Cheb1DParams cheb_params(const pf_ctx* c) {
       constexpr int NT = 256, EPT = 4; SPP spp = sine_params(ctx); __VA_ARGS__; } break; \
     case V_CHEB_128_1: { using SP = pf::Cheb1D<128, 1>; using SPP = pf::Cheb1DParams; \
       constexpr int NT = 128, EPT = 1; SPP spp = cheb_params(ctx); __VA_ARGS__; } break; \
+    case V_CHEB_512_1: { using SP = pf::Cheb1D<512, 1>; using SPP = pf::Cheb1DParams; \
+      constexpr int NT = 512, EPT = 1; SPP spp = cheb_params(ctx); __VA_ARGS__; } break; \
     default: \
       return set_error(ctx, PF_ERR_UNSUPPORTED, "no kernel variant"); \
   }
@@ -297,6 +319,7 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
   if (const char* ft = std::getenv("PF_FAR_TC")) far_tc = (ft[0] == '1') ? 1 : (ft[0] == '2') ? 2 : 0;
   const size_t scr_stride = (size_t)2 * (hps + 1) * 2 * pf::HB * c->size + parts_len;
   if (c->scratch.ensure((size_t)cap * scr_stride)) return cuda_fail(c, cudaErrorMemoryAllocation, "scratch");
+  if (ensure_cheb_aug(c, (size_t)cap)) return cuda_fail(c, cudaErrorMemoryAllocation, "chebyshev systems");
   // sync words: progress[cap] | ready[cap * hps] | abort[cap] | tickets[cap * 64]
   const int nsync = cap * (2 + hps) + cap * 64;
   if (c->sync_cap < nsync) {
@@ -341,6 +364,7 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
     int nl = n_lo + s0;
     PF_DISPATCH(c, {
       auto kern = pf::k_fine_sweep<SP, SPP, NT, EPT>;
+      offset_slab(spp, q0);
       int per_sm = 0;
       // shared-memory ring of the last NR states behind the space's own smem
       const size_t ring_bytes = sizeof(double) * pf::NR * c->size;
@@ -424,8 +448,12 @@ int launch_fine(pf_ctx* c, const double* d_u, int n_lo, int bs, double* d_out, S
 
 int launch_coarse(pf_ctx* c, const pf::CoarseArgs& a, Status* d_st) {
   pf::Common cm = make_common(c);
+  if (c->variant == V_CHEB_512_1 &&
+      c->cheb_aug_coarse.ensure((size_t)c->ni * pf::Cheb1D<512, 1>::ld_of(c->ni)))
+    return cuda_fail(c, cudaErrorMemoryAllocation, "chebyshev system");
   PF_DISPATCH(c, {
     auto kern = pf::k_coarse<SP, SPP, NT, EPT>;
+    coarse_slab(spp, c);
     PF_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
     kern<<<1, NT, c->smem, c->stream>>>(cm, spp, a, d_st);
   });
@@ -631,9 +659,14 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
     c->ni = deg - 1;
     c->size = c->ni;
     c->smem = pf::Cheb1D<128, 1>::smem_bytes(deg);
-    if (c->ni > 128 || c->smem > 227 * 1024)
-      return set_error(c, PF_ERR_UNSUPPORTED, "Chebyshev bridge supports degree <= ~100 (shared-memory resident)");
     c->variant = V_CHEB_128_1;
+    if (c->ni > 128 || c->smem > 227 * 1024) {
+      // the reference's own sizes (config 3: degree 513): D1 and the systems in global memory
+      if (c->ni > 512)
+        return set_error(c, PF_ERR_UNSUPPORTED, "Chebyshev bridge supports degree <= 513");
+      c->smem = pf::Cheb1D<512, 1>::smem_bytes(deg, true);
+      c->variant = V_CHEB_512_1;
+    }
     c->h_nodes.assign(space->nodes, space->nodes + c->npts);
     c->h_d1.assign(space->d1, space->d1 + (size_t)c->npts * c->npts);
     c->h_qw.assign(space->quad_weights, space->quad_weights + c->npts);
@@ -810,6 +843,8 @@ void pf_destroy(pf_ctx* c) {
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   if (c->side_stream) cudaStreamDestroy(c->side_stream);
   c->fold2.release();
+  c->cheb_aug.release();
+  c->cheb_aug_coarse.release();
   for (void* p : {(void*)c->d_status2, (void*)c->d_corr_status, (void*)c->d_corr_state, (void*)c->d_cancel})
     if (p) cudaFree(p);
   for (cudaStream_t s : c->pstream)

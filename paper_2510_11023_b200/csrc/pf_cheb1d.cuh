@@ -8,6 +8,12 @@
 //   LU with partial pivoting (virtual row permutation, reciprocal-pivot
 //   scaling as LAPACK dgetf2), pivot check |u_kk| > 1e-14 max|system|
 //   (stepping.py:62-75), back substitution.
+//
+// Two residences of the same algorithm: degree <= ~100 keeps D1 and the augmented
+// system in shared memory (Cheb1D<128, 1>); above that (the reference's own config-3
+// size, degree 513: a 512 x 513 system, 2 MB) D1 stays in global memory (L2-resident,
+// shared by every slice) and each CTA's system lives in its own global scratch slab
+// (Cheb1D<512, 1>, Cheb1DParams::aug_g).
 #pragma once
 #include "pf_device.cuh"
 
@@ -18,6 +24,8 @@ struct Cheb1DParams {
   const double* nodes;  // npts
   const double* d1;     // npts*npts
   const double* qw;     // npts
+  double* aug_g;        // global-memory residence: one ni x ld_of(ni) slab per CTA (nullptr: shared memory)
+  size_t aug_stride;    // doubles between the slabs of consecutive CTAs
 };
 
 template <int NT, int EPT>
@@ -38,21 +46,23 @@ struct Cheb1D {
     if ((ld & 1) == 0) ld += 1;
     return ld;
   }
-  static size_t smem_bytes(int degree) {
+  static size_t smem_bytes(int degree, bool global_residence = false) {
     const size_t npts = degree + 1, ni = degree - 1, ld = ld_of((int)ni);
-    return sizeof(double) * (npts * npts + 2 * npts + ni * ld + 3 * npts + ni + 5 + RED_DOUBLES) + sizeof(int) * (ni + 4);
+    const size_t mats = global_residence ? 0 : npts * npts + ni * ld;
+    return sizeof(double) * (mats + 2 * npts + 3 * npts + ni + 5 + RED_DOUBLES) + sizeof(int) * (ni + 4);
   }
 
   __device__ void init(char* smem, const Cheb1DParams& p) {
     npts = p.npts;
     ni = p.ni;
     LD = ld_of(ni);
+    const bool glob = p.aug_g != nullptr;
     double* s = reinterpret_cast<double*>(smem);
     double* d1s = s;
-    double* nds = d1s + npts * npts;
+    double* nds = glob ? s : d1s + npts * npts;
     double* qws = nds + npts;
-    aug = qws + npts;
-    uf = aug + ni * LD;
+    aug = glob ? p.aug_g + (size_t)blockIdx.x * p.aug_stride : qws + npts;
+    uf = glob ? qws + npts : aug + ni * LD;
     dv = uf + npts;
     xs = dv + npts;
     pivs = xs + npts;
@@ -60,13 +70,14 @@ struct Cheb1D {
     if (reinterpret_cast<uintptr_t>(rs) & 15) rs += 1;  // the reducer reads its slots as 16-byte pairs
     red.init(rs);
     perm = reinterpret_cast<int*>(rs + RED_DOUBLES);
-    for (int i = threadIdx.x; i < npts * npts; i += NT) d1s[i] = p.d1[i];
+    if (!glob)
+      for (int i = threadIdx.x; i < npts * npts; i += NT) d1s[i] = p.d1[i];
     for (int i = threadIdx.x; i < npts; i += NT) {
       nds[i] = p.nodes[i];
       qws[i] = p.qw[i];
       uf[i] = 0.0;
     }
-    d1 = d1s;
+    d1 = glob ? p.d1 : d1s;
     nodes = nds;
     qw = qws;
     __syncthreads();
