@@ -737,7 +737,9 @@ int pf_create(const pf_problem* problem, const pf_grid* grid, const pf_space* sp
     // (development aid for re-tuning)
     // (round 2 rescan on the device, tools/r02/sched_scan.py: order 7 lost to 6 once the states
     // carry the PCG tolerance's noise; config-3 sweep 7.18 -> 7.06 ms)
-    std::vector<long> sched = {5, 16, 6, 64, 5, 192, 4};
+    // (beyond a slice's 1024 substeps only the sequential solver reads the table: lower orders as
+    // the noise of its 65 536-row history grows, 0.628 -> 0.595 s at config 3)
+    std::vector<long> sched = {5, 16, 6, 64, 5, 192, 4, 1024, 3, 4096, 2};
     if (const char* es = std::getenv("PF_EXT_SCHED")) {
       sched.clear();
       for (const char* q = es; *q;) {
