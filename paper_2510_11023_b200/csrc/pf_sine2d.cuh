@@ -1033,8 +1033,17 @@ __global__ void k2_zero_fix(Sine2DArgs a) {
 #ifndef PF_HB2
 #define PF_HB2 8
 #endif
-// block length of the 2-D blocked history (k2_far every HB2 substeps; near rows < 2 HB2 in k2_prep)
+// block length of the 2-D blocked history (k2_far every HB2 substeps; near rows < HB2 in k2_prep)
 constexpr int HB2 = PF_HB2;
+// Rows folded into the far part of block beta: j <= (beta - PF_LAG2D) HB2.  The 2-D sweep runs in
+// lock-step on one stream, so nothing overlaps k2_far and the far part can reach the block's own
+// first row (lag 0: k2_prep reads 0..7 near rows per substep instead of 8..15; round 1 carried the
+// 1-D helper's one-block lag over).  Every sum still takes its rows in ascending order, so the
+// history is bitwise the same for either lag.
+#ifndef PF_LAG2D
+#define PF_LAG2D 0
+#endif
+__host__ __device__ constexpr int far_extent2(int beta) { return (beta > PF_LAG2D ? beta - PF_LAG2D : 0) * HB2; }
 #ifndef PF_TAU2D_R
 #define PF_TAU2D_R 32  // substeps of a slice extrapolated in local tau (k2_prep; 16-128 measured, 32 best)
 #endif
@@ -1064,7 +1073,7 @@ __global__ void __launch_bounds__(NT) k2_far(Hist2DArgs h, int beta) {
   const int e0 = blockIdx.x * NT * EPT;
   const size_t MM = h.MM;
   const int R0 = beta * HB2;
-  const int J = (beta > 0 ? beta - 1 : 0) * HB2;
+  const int J = far_extent2(beta);
   const double* path = h.paths + (size_t)b * (h.m + 1) * MM;
   double acc[HB2][EPT], cb[HB2][EPT];
   double c0[EPT];
@@ -1155,7 +1164,7 @@ __global__ void k2_prep(Hist2DArgs h, int r, double* HIST, double* CON, double* 
   const int b = blockIdx.y;
   const size_t MM = h.MM;
   const int rr = (r - 1) % HB2, beta = (r - 1) / HB2;
-  const int J = (beta > 0 ? beta - 1 : 0) * HB2;
+  const int J = far_extent2(beta);
   const int p = r - 1 < PF_EXO2 ? r - 1 : PF_EXO2;  // polynomial guess order after the local-tau range
   const double* path = h.paths + (size_t)b * (h.m + 1) * MM;
   const double* far = h.far + (size_t)b * 2 * HB2 * MM;
